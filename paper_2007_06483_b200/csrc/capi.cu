@@ -1,0 +1,152 @@
+// C-ABI plumbing: error state, launch accounting, pyramid planning and the
+// fused preprocess entry point (pipeline.py:80-85 on the device).
+#include <cstring>
+
+#include "common.cuh"
+
+namespace mtb {
+
+static thread_local std::string t_last_error;
+std::atomic<uint64_t> g_launches{0};
+
+void set_error(const std::string& msg) { t_last_error = msg; }
+void clear_error() { t_last_error.clear(); }
+
+int check_launch(const char* what, int n_launches) {
+  g_launches.fetch_add((uint64_t)n_launches, std::memory_order_relaxed);
+  const cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) {
+    set_error(std::string(what) + ": " + cudaGetErrorString(e));
+    return MTB_ECUDA;
+  }
+  return MTB_OK;
+}
+
+static int g_sms = 0;
+int num_sms() {
+  if (g_sms == 0) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    int v = 0;
+    if (cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || v <= 0) {
+      cudaGetLastError();
+      v = 148;
+    }
+    g_sms = v;
+  }
+  return g_sms;
+}
+
+bool make_plan(int w, int h, int requested, Plan* p) {
+  if (requested < 1 || w < kMinLevelSize || h < kMinLevelSize) return false;
+  const int ml = max_levels(w, h);
+  const int n = requested < ml ? requested : ml;
+  if (n > kMaxLevels) return false;
+  std::memset(p, 0, sizeof(*p));
+  p->n = n;
+  int64_t goff = 0, boff = 0;
+  for (int k = 0; k < n; ++k) {
+    LevelGeom& L = p->lv[k];
+    L.w = w >> k;
+    L.h = h >> k;
+    L.gray_pitch = round_up(L.w, 64);
+    L.gray_off = goff;
+    goff = round_up(goff + L.gray_pitch * L.h, 256);
+    L.nw64 = (L.w + 63) / 64;
+    L.bit_off = boff;
+    boff = round_up(boff + L.nw64 * L.h, 32);
+  }
+  p->gray_img_bytes = goff;
+  p->bit_img_words = boff;
+  return true;
+}
+
+// Defined in pyramid.cu / threshold.cu.
+int64_t spread_hist_elems(int n_levels);
+int launch_pyramid(const uint8_t* rgb, int64_t rgb_pitch, int64_t rgb_img_stride, int n_img, const Plan& p,
+                   uint8_t* gray, uint32_t* spread_hist, cudaStream_t st);
+int launch_hist_median(const uint32_t* spread_hist, int n_img, int n_levels, uint32_t* dense, int32_t* medians,
+                       cudaStream_t st);
+int launch_threshold_levels(const uint8_t* gray, const Plan& p, int n_img, const int32_t* medians, int tol,
+                            uint64_t* mtb, uint64_t* excl, cudaStream_t st);
+
+}  // namespace mtb
+
+using namespace mtb;
+
+extern "C" const char* mtb_last_error(void) { return t_last_error.c_str(); }
+extern "C" int mtb_abi_version(void) { return 1; }
+extern "C" uint64_t mtb_launch_count(void) { return g_launches.load(); }
+
+extern "C" int mtb_plan_levels(int w, int h, int requested, int64_t* geom, int64_t* sizes) {
+  Plan p;
+  if (!make_plan(w, h, requested, &p)) return -1;
+  if (geom) {
+    for (int k = 0; k < kMaxLevels; ++k) {
+      int64_t* g = geom + 6 * k;
+      if (k < p.n) {
+        g[0] = p.lv[k].w;
+        g[1] = p.lv[k].h;
+        g[2] = p.lv[k].gray_pitch;
+        g[3] = p.lv[k].gray_off;
+        g[4] = p.lv[k].nw64;
+        g[5] = p.lv[k].bit_off;
+      } else {
+        for (int i = 0; i < 6; ++i) g[i] = 0;
+      }
+    }
+  }
+  if (sizes) {
+    sizes[0] = p.gray_img_bytes;
+    sizes[1] = p.bit_img_words;
+    sizes[2] = spread_hist_elems(p.n);
+  }
+  return p.n;
+}
+
+extern "C" int mtb_pyramid_hist(const uint8_t* rgb, int64_t rgb_pitch, int64_t rgb_img_stride, int w, int h,
+                                int n_img, int levels, uint8_t* gray, uint32_t* hist_ws, void* stream) {
+  clear_error();
+  MTB_REQUIRE(rgb && gray && hist_ws, "null pointer");
+  MTB_REQUIRE(n_img >= 1 && n_img <= 65535, "image count out of range");
+  MTB_REQUIRE(rgb_pitch >= 3 * (int64_t)w, "rgb pitch smaller than row");
+  MTB_REQUIRE((int64_t)w * h < (int64_t)4294967295LL, "image too large for 32-bit histograms");
+  Plan p;
+  MTB_REQUIRE(make_plan(w, h, levels, &p), "image must be at least 16x16 and levels >= 1");
+  cudaStream_t st = as_stream(stream);
+  MTB_CUDA(cudaMemsetAsync(hist_ws, 0, sizeof(uint32_t) * spread_hist_elems(p.n) * n_img, st));
+  return launch_pyramid(rgb, rgb_pitch, rgb_img_stride, n_img, p, gray, hist_ws, st);
+}
+
+extern "C" int mtb_threshold_levels(const uint8_t* gray, const uint32_t* hist_ws, int w, int h, int n_img,
+                                    int levels, int tol, uint32_t* hist_out, int32_t* medians, uint64_t* mtb,
+                                    uint64_t* exclusion, void* stream) {
+  clear_error();
+  MTB_REQUIRE(gray && hist_ws && medians && mtb && exclusion, "null pointer");
+  MTB_REQUIRE(n_img >= 1 && n_img <= 65535, "image count out of range");
+  Plan p;
+  MTB_REQUIRE(make_plan(w, h, levels, &p), "image must be at least 16x16 and levels >= 1");
+  cudaStream_t st = as_stream(stream);
+  int rc = launch_hist_median(hist_ws, n_img, p.n, hist_out, medians, st);
+  if (rc) return rc;
+  return launch_threshold_levels(gray, p, n_img, medians, tol, mtb, exclusion, st);
+}
+
+extern "C" int mtb_preprocess(const uint8_t* rgb, int64_t rgb_pitch, int64_t rgb_img_stride, int w, int h,
+                              int n_img, int levels, int tol, uint8_t* gray, uint32_t* hist_ws, uint32_t* hist_out,
+                              int32_t* medians, uint64_t* mtb, uint64_t* exclusion, void* stream) {
+  clear_error();
+  MTB_REQUIRE(rgb && gray && hist_ws && medians && mtb && exclusion, "null pointer");
+  MTB_REQUIRE(n_img >= 1 && n_img <= 65535, "image count out of range");
+  MTB_REQUIRE(rgb_pitch >= 3 * (int64_t)w, "rgb pitch smaller than row");
+  MTB_REQUIRE((int64_t)w * h < (int64_t)4294967295LL, "image too large for 32-bit histograms");
+  Plan p;
+  MTB_REQUIRE(make_plan(w, h, levels, &p), "image must be at least 16x16 and levels >= 1");
+  cudaStream_t st = as_stream(stream);
+  MTB_CUDA(cudaMemsetAsync(hist_ws, 0, sizeof(uint32_t) * spread_hist_elems(p.n) * n_img, st));
+  int rc = launch_pyramid(rgb, rgb_pitch, rgb_img_stride, n_img, p, gray, hist_ws, st);
+  if (rc) return rc;
+  rc = launch_hist_median(hist_ws, n_img, p.n, hist_out, medians, st);
+  if (rc) return rc;
+  return launch_threshold_levels(gray, p, n_img, medians, tol, mtb, exclusion, st);
+}

@@ -1,0 +1,343 @@
+// K4: the shifted XOR/AND/popcount error test and the coarse-to-fine level
+// search, on packed bitmaps.
+//
+// Reference semantics (bit-exact):
+//   err(dx, dy) = sum over the row overlap 0 <= y-dy < h of
+//                 popcount((A[y] ^ S(B[y-dy], dx)) & EA[y] & S(EB[y-dy], dx))
+//   where S shifts a packed row toward higher x by dx bits with zero fill
+//   (kernels/_native.pyx:50-111, fallback.py:24-81, conftest.py:14-24).
+//   search_level: 9 candidates base + (ddx, ddy), (ddy, ddx) row-major over
+//   {-1,0,1}^2, winner minimises (err, |ddx|+|ddy|, index)   search.py:20-23,53-71
+//   find_offset: deepest level first, base = 2 * previous   search.py:74-95
+#include "common.cuh"
+
+namespace mtb {
+
+// Word idx of a packed row (u32 view), zero outside [0, nw32).
+__device__ __forceinline__ uint32_t row_word(const uint32_t* row, int64_t idx, int nw32) {
+  return (idx >= 0 && idx < nw32) ? __ldg(row + idx) : 0u;
+}
+
+// ----------------------------------------------------- generic K-candidate --
+// errs[k] += shifted_error(a, ea, b, eb, offsets[k]); one grid.y slice per k.
+__global__ void __launch_bounds__(256)
+shifted_error_multi_kernel(const uint32_t* __restrict__ a, const uint32_t* __restrict__ ea,
+                           const uint32_t* __restrict__ b, const uint32_t* __restrict__ eb, int64_t h, int nw32,
+                           const int32_t* __restrict__ offsets, int64_t dx0, int64_t dy0,
+                           unsigned long long* __restrict__ errs) {
+  // offsets == nullptr: a single candidate (dx0, dy0) passed by value.
+  const int k = blockIdx.y;
+  const int64_t dx = offsets ? (int64_t)offsets[2 * k] : dx0;
+  const int64_t dy = offsets ? (int64_t)offsets[2 * k + 1] : dy0;
+  const int64_t y0 = dy > 0 ? dy : 0;
+  const int64_t y1 = h + (dy < 0 ? dy : 0);
+  unsigned c = 0;
+  if (y1 > y0) {
+    const int64_t q = dx >> 5;  // floor division (arithmetic shift)
+    const int r = (int)(dx & 31);
+    const int64_t n = (y1 - y0) * nw32;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+      const int64_t yy = i / nw32;
+      const int j = (int)(i - yy * nw32);
+      const int64_t y = y0 + yy, sy = y - dy;
+      const uint32_t* brow = b + sy * nw32;
+      const uint32_t* erow = eb + sy * nw32;
+      const uint32_t bs = shifted_word(row_word(brow, j - q - 1, nw32), row_word(brow, j - q, nw32), r);
+      const uint32_t es = shifted_word(row_word(erow, j - q - 1, nw32), row_word(erow, j - q, nw32), r);
+      c += __popc((__ldg(a + y * nw32 + j) ^ bs) & __ldg(ea + y * nw32 + j) & es);
+    }
+  }
+  c = warp_sum(c);
+  if ((threadIdx.x & 31) == 0 && c) atomicAdd(&errs[k], (unsigned long long)c);
+}
+
+__global__ void shifted_error_bytemap_kernel(const uint8_t* __restrict__ a, const uint8_t* __restrict__ ea,
+                                             const uint8_t* __restrict__ b, const uint8_t* __restrict__ eb,
+                                             int64_t h, int64_t w, int64_t pitch, int64_t dx, int64_t dy,
+                                             unsigned long long* out) {
+  const int64_t x0 = dx > 0 ? dx : 0, x1 = w + (dx < 0 ? dx : 0);
+  const int64_t y0 = dy > 0 ? dy : 0, y1 = h + (dy < 0 ? dy : 0);
+  unsigned c = 0;
+  if (x1 > x0 && y1 > y0) {
+    const int64_t ow = x1 - x0, n = ow * (y1 - y0);
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+      const int64_t y = y0 + i / ow, x = x0 + i % ow;
+      const int64_t s = (y - dy) * pitch + (x - dx), d = y * pitch + x;
+      c += ((a[d] ^ b[s]) & ea[d] & eb[s]) != 0;
+    }
+  }
+  c = warp_sum(c);
+  if ((threadIdx.x & 31) == 0 && c) atomicAdd(out, (unsigned long long)c);
+}
+
+// The search.py:67 key, on (err, |ddx|+|ddy|, index).
+__device__ __forceinline__ bool key_less(unsigned long long e, int d, int i, unsigned long long be, int bd, int bi) {
+  if (e != be) return e < be;
+  if (d != bd) return d < bd;
+  return i < bi;
+}
+
+__global__ void select_candidate_kernel(const unsigned long long* errs, const int32_t* offsets, int k, int bdx,
+                                        int bdy, int32_t* chosen) {
+  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  int best = 0;
+  unsigned long long be = errs[0];
+  int bd = abs(offsets[0] - bdx) + abs(offsets[1] - bdy);
+  for (int i = 1; i < k; ++i) {
+    const unsigned long long e = errs[i];
+    const int d = abs(offsets[2 * i] - bdx) + abs(offsets[2 * i + 1] - bdy);
+    if (key_less(e, d, i, be, bd, best)) { best = i; be = e; bd = d; }
+  }
+  chosen[0] = offsets[2 * best];
+  chosen[1] = offsets[2 * best + 1];
+  chosen[2] = best;
+}
+
+// ----------------------------------------------------------- level search --
+constexpr int kSearchWarps = 4;
+constexpr int kSearchRows = 8;   // rows per warp strip
+
+struct LevelSearchArgs {
+  const uint64_t* const* maps;   // [P][4] {ref.mtb, ref.excl, tgt.mtb, tgt.excl}
+  int w, h, nw32;
+  const int32_t* prev;           // previous (coarser) level's chosen offset, or nullptr
+  int64_t prev_stride;
+  const int32_t* base;           // explicit base [P][2] when prev == nullptr (may be nullptr)
+  int32_t* acc;
+  int64_t acc_stride;
+  unsigned long long* errs;
+  int64_t errs_stride;
+  uint32_t* done;
+  int64_t done_stride;
+  int chunks;                    // ceil(nw32 / 32)
+};
+
+struct ShiftedRow {
+  uint32_t b[3], e[3];           // row shifted by bx-1, bx, bx+1
+};
+
+__device__ __forceinline__ ShiftedRow load_shifted(const uint32_t* bm, const uint32_t* em, int64_t sy, int h,
+                                                   int nw32, int64_t j, int qb, const int (&o)[3],
+                                                   const int (&r)[3]) {
+  ShiftedRow s;
+  uint32_t wb[4] = {0, 0, 0, 0}, we[4] = {0, 0, 0, 0};
+  if (sy >= 0 && sy < h && j < nw32) {
+    const uint32_t* br = bm + sy * nw32;
+    const uint32_t* er = em + sy * nw32;
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const int64_t idx = j - qb - 2 + i;  // W[j-qb-2 .. j-qb+1]
+      wb[i] = row_word(br, idx, nw32);
+      we[i] = row_word(er, idx, nw32);
+    }
+  }
+#pragma unroll
+  for (int d = 0; d < 3; ++d) {
+    // W[j-q] = w[2-o], W[j-q-1] = w[1-o] with o = q - qb in {-1, 0, 1}
+    const uint32_t hb = o[d] < 0 ? wb[3] : (o[d] == 0 ? wb[2] : wb[1]);
+    const uint32_t lb = o[d] < 0 ? wb[2] : (o[d] == 0 ? wb[1] : wb[0]);
+    const uint32_t he = o[d] < 0 ? we[3] : (o[d] == 0 ? we[2] : we[1]);
+    const uint32_t le = o[d] < 0 ? we[2] : (o[d] == 0 ? we[1] : we[0]);
+    s.b[d] = shifted_word(lb, hb, r[d]);
+    s.e[d] = shifted_word(le, he, r[d]);
+  }
+  return s;
+}
+
+__global__ void __launch_bounds__(kSearchWarps * 32)
+level_search_kernel(LevelSearchArgs a) {
+  __shared__ unsigned s_part[kSearchWarps][9];
+  __shared__ int s_last;
+  const int p = blockIdx.y;
+  const int lane = threadIdx.x & 31, wi = threadIdx.x >> 5;
+  const int chunk = blockIdx.x % a.chunks, group = blockIdx.x / a.chunks;
+  const uint32_t* A = reinterpret_cast<const uint32_t*>(a.maps[4 * p + 0]);
+  const uint32_t* EA = reinterpret_cast<const uint32_t*>(a.maps[4 * p + 1]);
+  const uint32_t* B = reinterpret_cast<const uint32_t*>(a.maps[4 * p + 2]);
+  const uint32_t* EB = reinterpret_cast<const uint32_t*>(a.maps[4 * p + 3]);
+
+  int bx = 0, by = 0;
+  if (a.prev) {
+    bx = 2 * a.prev[p * a.prev_stride];
+    by = 2 * a.prev[p * a.prev_stride + 1];
+  } else if (a.base) {
+    bx = a.base[2 * p];
+    by = a.base[2 * p + 1];
+  }
+  const int qb = bx >> 5;
+  int o[3], r[3];
+#pragma unroll
+  for (int d = 0; d < 3; ++d) {
+    const int dx = bx + d - 1;
+    o[d] = (dx >> 5) - qb;
+    r[d] = dx & 31;
+  }
+
+  const int64_t j = (int64_t)chunk * 32 + lane;
+  const int y0 = (group * kSearchWarps + wi) * kSearchRows;
+  unsigned cnt[9];
+#pragma unroll
+  for (int i = 0; i < 9; ++i) cnt[i] = 0;
+
+  if (y0 < a.h) {
+    // Window of source rows y-by-1 (ddy=+1), y-by (ddy=0), y-by+1 (ddy=-1).
+    ShiftedRow w0 = load_shifted(B, EB, (int64_t)y0 - by - 1, a.h, a.nw32, j, qb, o, r);
+    ShiftedRow w1 = load_shifted(B, EB, (int64_t)y0 - by, a.h, a.nw32, j, qb, o, r);
+    for (int y = y0; y < y0 + kSearchRows && y < a.h; ++y) {
+      const ShiftedRow w2 = load_shifted(B, EB, (int64_t)y - by + 1, a.h, a.nw32, j, qb, o, r);
+      if (j < a.nw32) {
+        const uint32_t av = __ldg(A + (int64_t)y * a.nw32 + j);
+        const uint32_t ev = __ldg(EA + (int64_t)y * a.nw32 + j);
+#pragma unroll
+        for (int d = 0; d < 3; ++d) {
+          cnt[0 + d] += __popc((av ^ w2.b[d]) & ev & w2.e[d]);  // ddy = -1
+          cnt[3 + d] += __popc((av ^ w1.b[d]) & ev & w1.e[d]);  // ddy =  0
+          cnt[6 + d] += __popc((av ^ w0.b[d]) & ev & w0.e[d]);  // ddy = +1
+        }
+      }
+      w0 = w1;
+      w1 = w2;
+    }
+  }
+#pragma unroll
+  for (int i = 0; i < 9; ++i) {
+    const unsigned v = warp_sum(cnt[i]);
+    if (lane == 0) s_part[wi][i] = v;
+  }
+  __syncthreads();
+  unsigned long long* errs = a.errs + p * a.errs_stride;
+  if (threadIdx.x < 9) {
+    unsigned long long v = 0;
+#pragma unroll
+    for (int k = 0; k < kSearchWarps; ++k) v += s_part[k][threadIdx.x];
+    if (v) atomicAdd(&errs[threadIdx.x], v);
+  }
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) s_last = (atomicAdd(&a.done[p * a.done_stride], 1u) == gridDim.x - 1);
+  __syncthreads();
+  if (s_last && threadIdx.x == 0) {
+    __threadfence();
+    int best = 0;
+    unsigned long long be = 0;
+    int bd = 0;
+#pragma unroll
+    for (int i = 0; i < 9; ++i) {
+      const unsigned long long e = *((volatile unsigned long long*)&errs[i]);
+      const int ddy = i / 3 - 1, ddx = i % 3 - 1;
+      const int d = abs(ddx) + abs(ddy);
+      if (i == 0 || key_less(e, d, i, be, bd, best)) { best = i; be = e; bd = d; }
+    }
+    a.acc[p * a.acc_stride] = bx + best % 3 - 1;
+    a.acc[p * a.acc_stride + 1] = by + best / 3 - 1;
+  }
+}
+
+}  // namespace mtb
+
+using namespace mtb;
+
+extern "C" int mtb_shifted_error_packed(const uint64_t* a, const uint64_t* ea, const uint64_t* b, const uint64_t* eb,
+                                        int64_t h, int64_t nwords64, int64_t dx, int64_t dy, unsigned long long* out,
+                                        void* stream) {
+  clear_error();
+  MTB_REQUIRE(out, "null output pointer");
+  MTB_REQUIRE(h >= 0 && nwords64 >= 0, "negative dimensions");
+  MTB_CUDA(cudaMemsetAsync(out, 0, sizeof(unsigned long long), as_stream(stream)));
+  if (h == 0 || nwords64 == 0) return MTB_OK;
+  MTB_REQUIRE(a && ea && b && eb, "null bitmap pointer");
+  MTB_REQUIRE(nwords64 < (1 << 25), "row too wide");
+  const int64_t n = 2 * nwords64 * h;
+  shifted_error_multi_kernel<<<dim3(grid_cap(n, 256), 1), 256, 0, as_stream(stream)>>>(
+      reinterpret_cast<const uint32_t*>(a), reinterpret_cast<const uint32_t*>(ea),
+      reinterpret_cast<const uint32_t*>(b), reinterpret_cast<const uint32_t*>(eb), h, (int)(2 * nwords64), nullptr,
+      dx, dy, out);
+  return check_launch("shifted_error_multi_kernel");
+}
+
+extern "C" int mtb_shifted_error_multi(const uint64_t* a, const uint64_t* ea, const uint64_t* b, const uint64_t* eb,
+                                       int64_t h, int64_t nwords64, const int32_t* offsets, int k,
+                                       unsigned long long* errs, void* stream) {
+  clear_error();
+  MTB_REQUIRE(errs && offsets, "null pointer");
+  MTB_REQUIRE(k >= 1 && k <= 65535, "candidate count out of range");
+  MTB_REQUIRE(h >= 0 && nwords64 >= 0, "negative dimensions");
+  MTB_CUDA(cudaMemsetAsync(errs, 0, sizeof(unsigned long long) * k, as_stream(stream)));
+  if (h == 0 || nwords64 == 0) return MTB_OK;
+  MTB_REQUIRE(a && ea && b && eb, "null bitmap pointer");
+  const int64_t n = 2 * nwords64 * h;
+  int g = grid_cap(n, 256);
+  if (k > 1) {
+    g = (int)((int64_t)num_sms() * 8 / k);
+    if (g < 1) g = 1;
+    const int64_t need = (n + 255) / 256;
+    if (g > need) g = (int)need;
+  }
+  shifted_error_multi_kernel<<<dim3(g, k), 256, 0, as_stream(stream)>>>(
+      reinterpret_cast<const uint32_t*>(a), reinterpret_cast<const uint32_t*>(ea),
+      reinterpret_cast<const uint32_t*>(b), reinterpret_cast<const uint32_t*>(eb), h, (int)(2 * nwords64), offsets,
+      0, 0, errs);
+  return check_launch("shifted_error_multi_kernel");
+}
+
+extern "C" int mtb_shifted_error_bytemap(const uint8_t* a, const uint8_t* ea, const uint8_t* b, const uint8_t* eb,
+                                         int64_t h, int64_t w, int64_t pitch, int64_t dx, int64_t dy,
+                                         unsigned long long* out, void* stream) {
+  clear_error();
+  MTB_REQUIRE(out, "null output pointer");
+  MTB_REQUIRE(h >= 0 && w >= 0 && pitch >= w, "bad dimensions");
+  MTB_CUDA(cudaMemsetAsync(out, 0, sizeof(unsigned long long), as_stream(stream)));
+  if (h * w == 0) return MTB_OK;
+  MTB_REQUIRE(a && ea && b && eb, "null bitmap pointer");
+  shifted_error_bytemap_kernel<<<grid_cap(h * w, 256), 256, 0, as_stream(stream)>>>(a, ea, b, eb, h, w, pitch, dx, dy,
+                                                                                   out);
+  return check_launch("shifted_error_bytemap_kernel");
+}
+
+extern "C" int mtb_select_candidate(const unsigned long long* errs, const int32_t* offsets, int k, int base_dx,
+                                    int base_dy, int32_t* chosen, void* stream) {
+  clear_error();
+  MTB_REQUIRE(errs && offsets && chosen, "null pointer");
+  MTB_REQUIRE(k >= 1, "need at least one candidate");
+  select_candidate_kernel<<<1, 32, 0, as_stream(stream)>>>(errs, offsets, k, base_dx, base_dy, chosen);
+  return check_launch("select_candidate_kernel");
+}
+
+extern "C" int mtb_find_offset_batch(const uint64_t* const* maps, const int32_t* dims, int n_levels, int P,
+                                     const int32_t* base, int32_t* acc, unsigned long long* errs, uint32_t* done,
+                                     void* stream) {
+  clear_error();
+  MTB_REQUIRE(maps && dims && acc && errs && done, "null pointer");
+  MTB_REQUIRE(n_levels >= 1 && n_levels <= MTB_MAX_LEVELS, "level count out of range");
+  MTB_REQUIRE(P >= 1 && P <= 65535, "pair count out of range");
+  for (int k = 0; k < n_levels; ++k) {
+    MTB_REQUIRE(dims[3 * k] >= 1 && dims[3 * k + 1] >= 1, "level dimensions must be positive");
+    MTB_REQUIRE((int64_t)dims[3 * k + 2] * 64 >= dims[3 * k], "row word count too small for width");
+  }
+  cudaStream_t st = as_stream(stream);
+  MTB_CUDA(cudaMemsetAsync(errs, 0, sizeof(unsigned long long) * 9 * n_levels * P, st));
+  MTB_CUDA(cudaMemsetAsync(done, 0, sizeof(uint32_t) * n_levels * P, st));
+  int launches = 0;
+  for (int k = n_levels - 1; k >= 0; --k) {
+    LevelSearchArgs a{};
+    a.maps = maps + (int64_t)k * P * 4;
+    a.w = dims[3 * k];
+    a.h = dims[3 * k + 1];
+    a.nw32 = 2 * dims[3 * k + 2];
+    a.prev = (k == n_levels - 1) ? nullptr : acc + 2 * (k + 1);
+    a.prev_stride = 2 * n_levels;
+    a.base = base;
+    a.acc = acc + 2 * k;
+    a.acc_stride = 2 * n_levels;
+    a.errs = errs + 9 * k;
+    a.errs_stride = 9 * n_levels;
+    a.done = done + k;
+    a.done_stride = n_levels;
+    a.chunks = (a.nw32 + 31) / 32;
+    const int rows_per_cta = kSearchWarps * kSearchRows;
+    const int groups = (a.h + rows_per_cta - 1) / rows_per_cta;
+    level_search_kernel<<<dim3(a.chunks * groups, P), kSearchWarps * 32, 0, st>>>(a);
+    ++launches;
+  }
+  return check_launch("level_search_kernel", launches);
+}

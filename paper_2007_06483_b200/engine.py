@@ -1,0 +1,222 @@
+"""Batched, device-resident MTB engine: the fused hot path.
+
+One `MtbEngine` serves images of one size and one (levels, tol) setting.
+`preprocess` runs to_grayscale -> build_pyramid -> build_mtb_pyramid for a
+whole batch of RGB images in three kernels (pipeline.py:80-85 fused; see
+csrc/pyramid.cu, csrc/threshold.cu).  `search` runs find_offset for any
+number of (reference, target) image pairs with every level on the device
+(search.py:74-95; csrc/search.cu): the offset chosen at one level feeds the
+next through device memory, so nothing returns to the host until the caller
+reads the results.
+
+Arena layout in HBM (per image, from mtb_plan_levels):
+  gray    level k at gray_off[k], row pitch round_up(w_k, 64) bytes
+  bitmaps level k at bit_off[k] u64 words, ceil(w_k/64) words per row —
+          the reference's packed layout (bitmap.py:32-40), one arena for the
+          MTBs and one for the exclusion maps.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import _dev, _lib
+from .bitmap import PACKED, Bitmap
+from .image import ShiftOffset
+from .instrumentation import (FIND_OFFSET_CALLS, MTB_PYRAMID_BUILDS, PYRAMID_BUILDS, SHIFTED_ERROR_EVALS,
+                              counters)
+from .search import NEIGHBORHOOD, AlignmentResult, LevelTrace
+from .threshold import MtbPair
+
+
+@dataclass
+class PyramidSet:
+    """Device arenas holding the MTB pyramids of a batch of images."""
+
+    n_img: int
+    gray: "object"        # uint8 [n_img, gray_image_bytes]
+    hist_ws: "object"     # int32 [n_img, hist_ws_elems] (spread histograms)
+    hist: "object"        # int32 [n_img, n, 256] dense histograms (or None)
+    medians: "object"     # int32 [n_img, n]
+    mtb: "object"         # int64 [n_img, bitmap_image_words]
+    excl: "object"        # int64 [n_img, bitmap_image_words]
+
+
+class MtbEngine:
+    def __init__(self, width: int, height: int, levels: int = 6, tol: int = 4):
+        self.torch = _dev.torch_mod()
+        plan = _lib.plan_levels(width, height, levels)
+        if plan is None:
+            raise ValueError(f"images must be at least 16x16 and levels >= 1; got {width}x{height}, {levels}")
+        self.width, self.height, self.requested_levels, self.tol = int(width), int(height), int(levels), int(tol)
+        self.n, self.geom, sizes = plan
+        self.gray_img_bytes = int(sizes[0])
+        self.bit_img_words = int(sizes[1])
+        self.hist_ws_elems = int(sizes[2])
+        self.dims = np.ascontiguousarray(
+            np.stack([self.geom[:, 0], self.geom[:, 1], self.geom[:, 4]], axis=1).astype(np.int32))
+        self._tables = {}
+
+    # ------------------------------------------------------------ buffers --
+    def alloc(self, n_img: int, keep_hist: bool = False) -> PyramidSet:
+        t = self.torch
+        return PyramidSet(
+            n_img=n_img,
+            gray=t.empty((n_img, self.gray_img_bytes), dtype=t.uint8, device="cuda"),
+            hist_ws=t.empty((n_img, self.hist_ws_elems), dtype=t.int32, device="cuda"),
+            hist=t.empty((n_img, self.n, 256), dtype=t.int32, device="cuda") if keep_hist else None,
+            medians=t.empty((n_img, self.n), dtype=t.int32, device="cuda"),
+            mtb=t.empty((n_img, self.bit_img_words), dtype=t.int64, device="cuda"),
+            excl=t.empty((n_img, self.bit_img_words), dtype=t.int64, device="cuda"),
+        )
+
+    def _check_rgb(self, rgb):
+        t = self.torch
+        if not (_dev.is_tensor(rgb) and rgb.is_cuda and rgb.dtype == t.uint8 and rgb.dim() == 4
+                and tuple(rgb.shape[1:]) == (self.height, self.width, 3)):
+            raise ValueError(f"expected a CUDA uint8 (N, {self.height}, {self.width}, 3) batch, got "
+                             f"{getattr(rgb, 'shape', None)} {getattr(rgb, 'dtype', None)}")
+        if not rgb.is_contiguous():
+            raise ValueError("RGB batch must be contiguous")
+
+    # ---------------------------------------------------------- preprocess --
+    def _ptrs(self, rgb, pyr: PyramidSet, i0: int):
+        """Device addresses of image i0 in the input batch and in every arena."""
+        img_bytes = 3 * self.width * self.height
+        return dict(
+            rgb=(_dev.ptr(rgb) + i0 * img_bytes) if rgb is not None else None,
+            gray=_dev.ptr(pyr.gray) + i0 * self.gray_img_bytes,
+            hist_ws=_dev.ptr(pyr.hist_ws) + i0 * self.hist_ws_elems * 4,
+            hist=(_dev.ptr(pyr.hist) + i0 * self.n * 256 * 4) if pyr.hist is not None else None,
+            medians=_dev.ptr(pyr.medians) + i0 * self.n * 4,
+            mtb=_dev.ptr(pyr.mtb) + i0 * self.bit_img_words * 8,
+            excl=_dev.ptr(pyr.excl) + i0 * self.bit_img_words * 8,
+        )
+
+    def pyramid_hist(self, rgb, pyr: PyramidSet, i0: int = 0, count: int | None = None):
+        """Stage 1: gray + pyramid + per-level histograms (one RGB pass) of images [i0, i0+count)."""
+        count = int(rgb.shape[0]) - i0 if count is None else count
+        p = self._ptrs(rgb, pyr, i0)
+        _lib.call("mtb_pyramid_hist", p["rgb"], 3 * self.width, 3 * self.width * self.height,
+                  self.width, self.height, count, self.requested_levels, p["gray"], p["hist_ws"], _dev.stream())
+
+    def threshold_levels(self, pyr: PyramidSet, n_img: int, i0: int = 0):
+        """Stage 2: medians + MTB/exclusion packing of every level of images [i0, i0+n_img)."""
+        p = self._ptrs(None, pyr, i0)
+        _lib.call("mtb_threshold_levels", p["gray"], p["hist_ws"], self.width, self.height,
+                  n_img, self.requested_levels, self.tol, p["hist"], p["medians"], p["mtb"], p["excl"],
+                  _dev.stream())
+
+    def preprocess_range(self, rgb, pyr: PyramidSet, i0: int, count: int):
+        """Fused preprocess (all three kernels) of images [i0, i0+count) into their arena slots."""
+        p = self._ptrs(rgb, pyr, i0)
+        _lib.call("mtb_preprocess", p["rgb"], 3 * self.width, 3 * self.width * self.height, self.width,
+                  self.height, count, self.requested_levels, self.tol, p["gray"], p["hist_ws"], p["hist"],
+                  p["medians"], p["mtb"], p["excl"], _dev.stream())
+
+    def preprocess(self, rgb, pyr: PyramidSet | None = None, keep_hist: bool = False,
+                   count: bool = True) -> PyramidSet:
+        """MTB pyramids of an (N, H, W, 3) CUDA batch (pipeline.py:80-85 fused)."""
+        self._check_rgb(rgb)
+        n_img = int(rgb.shape[0])
+        if pyr is None:
+            pyr = self.alloc(n_img, keep_hist)
+        self.preprocess_range(rgb, pyr, 0, n_img)
+        if count:
+            counters.bump(PYRAMID_BUILDS, n_img)
+            counters.bump(MTB_PYRAMID_BUILDS, n_img)
+        return pyr
+
+    # ------------------------------------------------------------- views --
+    def gray_level(self, pyr: PyramidSet, img: int, k: int):
+        w, h, pitch, off = (int(v) for v in self.geom[k, :4])
+        return pyr.gray[img, off:off + pitch * h].view(h, pitch)[:, :w]
+
+    def bitmap_words(self, arena, img: int, k: int):
+        w, h, nw, off = int(self.geom[k, 0]), int(self.geom[k, 1]), int(self.geom[k, 4]), int(self.geom[k, 5])
+        return arena[img, off:off + nw * h].view(h, nw)
+
+    def mtb_pyramid(self, pyr: PyramidSet, img: int, layout: str = PACKED, medians=None) -> list:
+        """Reference-shaped list[MtbPair] views of one image's arena slices."""
+        if medians is None:
+            medians = pyr.medians[img].cpu().numpy()
+        out = []
+        for k in range(self.n):
+            w, h = int(self.geom[k, 0]), int(self.geom[k, 1])
+            out.append(MtbPair(mtb=Bitmap(w, h, layout, self.bitmap_words(pyr.mtb, img, k)),
+                               exclusion=Bitmap(w, h, layout, self.bitmap_words(pyr.excl, img, k)),
+                               median=int(medians[k]), noise_tolerance=self.tol))
+        return out
+
+    # --------------------------------------------------------------- search --
+    def maps_table(self, pyr: PyramidSet, pairs) -> "object":
+        """Device table [n][P][4] of level pointers {ref.mtb, ref.excl, tgt.mtb, tgt.excl}."""
+        pairs = np.asarray(pairs, dtype=np.int64).reshape(-1, 2)
+        key = (int(pyr.mtb.data_ptr()), int(pyr.excl.data_ptr()), pairs.tobytes())
+        tab = self._tables.get(key)
+        if tab is not None:
+            return tab
+        stride = self.bit_img_words * 8
+        offs = self.geom[:, 5].astype(np.int64) * 8                                  # [n]
+        m0, e0 = int(pyr.mtb.data_ptr()), int(pyr.excl.data_ptr())
+        ref, tgt = pairs[:, 0], pairs[:, 1]
+        table = np.empty((self.n, len(pairs), 4), dtype=np.int64)
+        table[:, :, 0] = m0 + ref[None, :] * stride + offs[:, None]
+        table[:, :, 1] = e0 + ref[None, :] * stride + offs[:, None]
+        table[:, :, 2] = m0 + tgt[None, :] * stride + offs[:, None]
+        table[:, :, 3] = e0 + tgt[None, :] * stride + offs[:, None]
+        tab = self.torch.from_numpy(table).to("cuda")
+        if len(self._tables) > 64:
+            self._tables.clear()
+        self._tables[key] = tab
+        return tab
+
+    def search_table(self, table, n_pairs: int, acc=None, errs=None, done=None, base=None, count: bool = True):
+        """find_offset for every pair of a prepared maps table; results stay on device.
+
+        Returns (acc [P, n, 2] int32 — chosen offset per level, index 0 = full
+        resolution; errs [P, n, 9] int64 — candidate errors per level).
+        """
+        t = self.torch
+        if acc is None:
+            acc = t.empty((n_pairs, self.n, 2), dtype=t.int32, device="cuda")
+        if errs is None:
+            errs = t.empty((n_pairs, self.n, 9), dtype=t.int64, device="cuda")
+        if done is None:
+            done = t.empty((n_pairs, self.n), dtype=t.int32, device="cuda")
+        _lib.call("mtb_find_offset_batch", _dev.ptr(table), self.dims.ctypes.data, self.n, n_pairs,
+                  _dev.ptr(base) if base is not None else None, _dev.ptr(acc), _dev.ptr(errs), _dev.ptr(done),
+                  _dev.stream())
+        if count:
+            counters.bump(FIND_OFFSET_CALLS, n_pairs)
+            counters.bump(SHIFTED_ERROR_EVALS, 9 * self.n * n_pairs)
+        return acc, errs
+
+    def search(self, pyr: PyramidSet, pairs, count: bool = True):
+        table = self.maps_table(pyr, pairs)
+        return self.search_table(table, int(table.shape[1]), count=count)
+
+
+def results_from_device(acc, errs, base=None) -> list[AlignmentResult]:
+    """AlignmentResult per pair (traces deepest first) from the device outputs."""
+    acc_h = acc.cpu().numpy()
+    errs_h = errs.cpu().numpy()
+    out = []
+    for p in range(acc_h.shape[0]):
+        n = acc_h.shape[1]
+        traces = []
+        prev = None
+        for level in reversed(range(n)):
+            if prev is None:
+                b = ShiftOffset(0, 0) if base is None else ShiftOffset(int(base[p][0]), int(base[p][1]))
+            else:
+                b = prev.scaled(2)
+            cands = [(ShiftOffset(b.dx + ddx, b.dy + ddy), int(errs_h[p, level, i]))
+                     for i, (ddy, ddx) in enumerate(NEIGHBORHOOD)]
+            chosen = ShiftOffset(int(acc_h[p, level, 0]), int(acc_h[p, level, 1]))
+            traces.append(LevelTrace(level=level, candidates=cands, chosen=chosen, accumulated=chosen))
+            prev = chosen
+        out.append(AlignmentResult(offset=prev, traces=traces, total_tests=9 * n))
+    return out
