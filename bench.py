@@ -50,7 +50,8 @@ def parse():
     ap.add_argument("--height", type=int, default=4000)
     ap.add_argument("--levels", type=int, default=6)
     ap.add_argument("--tol", type=int, default=4)
-    ap.add_argument("--chunk", type=int, default=0, help="images per preprocess launch (0 = whole batch)")
+    ap.add_argument("--chunk", type=int, default=2, help="images per preprocess launch pair (0 = whole batch)")
+    ap.add_argument("--keep-gray", action="store_true", help="do not discard consumed gray lines from L2")
     ap.add_argument("--e2e-steps", type=int, default=10)
     ap.add_argument("--cpu-reps", type=int, default=3)
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -233,7 +234,7 @@ def run_ours(args, rank, world, local_rank):
                 ev.append((s, e))
             else:
                 eng.pyramid_hist(batch, pyr, i0, c)
-            eng.threshold_levels(pyr, c, i0)
+            eng.threshold_levels(pyr, c, i0, discard_gray=not args.keep_gray)
         eng.search_table(table, P, acc, errs, done, count=False)
 
     for _ in range(max(3, args.warmup)):
@@ -285,6 +286,7 @@ def run_ours(args, rank, world, local_rank):
                                f"{args.levels} levels, tol {args.tol} (BASELINE config 2, batched)",
                    "width": args.width, "height": args.height, "levels": args.levels, "tol": args.tol,
                    "pairs_per_step_per_gpu": P, "preprocess_chunk_images": chunk,
+                   "discard_gray": not args.keep_gray,
                    "l2": f"inputs {n_img * img_bytes / 1e9:.2f} GB per step per GPU > 126 MB L2; no flush needed",
                    "parallelism": f"batch-shard dp{world} (no collective)",
                    "correct_offsets": f"{correct}/{P} match ground truth"},

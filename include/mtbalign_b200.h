@@ -189,13 +189,15 @@ int mtb_preprocess(const uint8_t* rgb, int64_t rgb_pitch, int64_t rgb_img_stride
 
 /* The two halves of mtb_preprocess, for per-stage timing (pipeline.py:77-85):
  * mtb_pyramid_hist = gray + pyramid + spread histograms (zeroes hist_ws);
- * mtb_threshold_levels = medians + threshold/pack of every level. */
+ * mtb_threshold_levels = medians + threshold/pack of every level; with
+ * discard_gray != 0 the gray lines it consumed are dropped from L2 without
+ * write-back (discard.global.L2), leaving the gray workspace undefined. */
 int mtb_pyramid_hist(const uint8_t* rgb, int64_t rgb_pitch, int64_t rgb_img_stride,
                      int w, int h, int n_img, int levels,
                      uint8_t* gray, uint32_t* hist_ws, void* stream);
 int mtb_threshold_levels(const uint8_t* gray, const uint32_t* hist_ws, int w, int h, int n_img,
                          int levels, int tol, uint32_t* hist_out, int32_t* medians,
-                         uint64_t* mtb, uint64_t* exclusion, void* stream);
+                         uint64_t* mtb, uint64_t* exclusion, int discard_gray, void* stream);
 
 /* Coarse-to-fine search (find_offset, search.py:74-95; per level
  * search_level, search.py:53-71) for P pairs at once, all levels on device.

@@ -48,7 +48,7 @@ SIGNATURES = {
     "mtb_select_candidate": [_c_void_p, _c_void_p, _i32, _i32, _i32, _c_void_p, _c_void_p],
     "mtb_pyramid_hist": [_c_void_p, _i64, _i64, _i32, _i32, _i32, _i32, _c_void_p, _c_void_p, _c_void_p],
     "mtb_threshold_levels": [_c_void_p, _c_void_p, _i32, _i32, _i32, _i32, _i32, _c_void_p, _c_void_p,
-                             _c_void_p, _c_void_p, _c_void_p],
+                             _c_void_p, _c_void_p, _i32, _c_void_p],
     "mtb_preprocess": [_c_void_p, _i64, _i64, _i32, _i32, _i32, _i32, _i32, _c_void_p, _c_void_p, _c_void_p,
                        _c_void_p, _c_void_p, _c_void_p, _c_void_p],
     "mtb_find_offset_batch": [_c_void_p, _c_void_p, _i32, _i32, _c_void_p, _c_void_p, _c_void_p, _c_void_p,

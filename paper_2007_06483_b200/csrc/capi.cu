@@ -49,7 +49,7 @@ bool make_plan(int w, int h, int requested, Plan* p) {
     LevelGeom& L = p->lv[k];
     L.w = w >> k;
     L.h = h >> k;
-    L.gray_pitch = round_up(L.w, 64);
+    L.gray_pitch = round_up(L.w, 128);
     L.gray_off = goff;
     goff = round_up(goff + L.gray_pitch * L.h, 256);
     L.nw64 = (L.w + 63) / 64;
@@ -68,7 +68,7 @@ int launch_pyramid(const uint8_t* rgb, int64_t rgb_pitch, int64_t rgb_img_stride
 int launch_hist_median(const uint32_t* spread_hist, int n_img, int n_levels, uint32_t* dense, int32_t* medians,
                        cudaStream_t st);
 int launch_threshold_levels(const uint8_t* gray, const Plan& p, int n_img, const int32_t* medians, int tol,
-                            uint64_t* mtb, uint64_t* excl, cudaStream_t st);
+                            uint64_t* mtb, uint64_t* excl, int discard, cudaStream_t st);
 
 }  // namespace mtb
 
@@ -120,22 +120,24 @@ extern "C" int mtb_pyramid_hist(const uint8_t* rgb, int64_t rgb_pitch, int64_t r
 
 extern "C" int mtb_threshold_levels(const uint8_t* gray, const uint32_t* hist_ws, int w, int h, int n_img,
                                     int levels, int tol, uint32_t* hist_out, int32_t* medians, uint64_t* mtb,
-                                    uint64_t* exclusion, void* stream) {
+                                    uint64_t* exclusion, int discard_gray, void* stream) {
   clear_error();
   MTB_REQUIRE(gray && hist_ws && medians && mtb && exclusion, "null pointer");
   MTB_REQUIRE(n_img >= 1 && n_img <= 65535, "image count out of range");
+  MTB_REQUIRE(tol >= 0 && tol <= 255, "noise tolerance must be in 0..255");
   Plan p;
   MTB_REQUIRE(make_plan(w, h, levels, &p), "image must be at least 16x16 and levels >= 1");
   cudaStream_t st = as_stream(stream);
   int rc = launch_hist_median(hist_ws, n_img, p.n, hist_out, medians, st);
   if (rc) return rc;
-  return launch_threshold_levels(gray, p, n_img, medians, tol, mtb, exclusion, st);
+  return launch_threshold_levels(gray, p, n_img, medians, tol, mtb, exclusion, discard_gray, st);
 }
 
 extern "C" int mtb_preprocess(const uint8_t* rgb, int64_t rgb_pitch, int64_t rgb_img_stride, int w, int h,
                               int n_img, int levels, int tol, uint8_t* gray, uint32_t* hist_ws, uint32_t* hist_out,
                               int32_t* medians, uint64_t* mtb, uint64_t* exclusion, void* stream) {
   clear_error();
+  MTB_REQUIRE(tol >= 0 && tol <= 255, "noise tolerance must be in 0..255");
   MTB_REQUIRE(rgb && gray && hist_ws && medians && mtb && exclusion, "null pointer");
   MTB_REQUIRE(n_img >= 1 && n_img <= 65535, "image count out of range");
   MTB_REQUIRE(rgb_pitch >= 3 * (int64_t)w, "rgb pitch smaller than row");
@@ -148,5 +150,5 @@ extern "C" int mtb_preprocess(const uint8_t* rgb, int64_t rgb_pitch, int64_t rgb
   if (rc) return rc;
   rc = launch_hist_median(hist_ws, n_img, p.n, hist_out, medians, st);
   if (rc) return rc;
-  return launch_threshold_levels(gray, p, n_img, medians, tol, mtb, exclusion, st);
+  return launch_threshold_levels(gray, p, n_img, medians, tol, mtb, exclusion, 0, st);
 }

@@ -57,7 +57,7 @@ constexpr int kMaxLevels = MTB_MAX_LEVELS;
 
 struct LevelGeom {
   int w, h;
-  int64_t gray_pitch;   // bytes, multiple of 64 (so one u32 word = 32 aligned bytes)
+  int64_t gray_pitch;   // bytes, multiple of 128 (one L2 line; a u32 bitmap word = 32 aligned bytes)
   int64_t gray_off;     // bytes from the image's gray arena base, 256-aligned
   int64_t nw64;         // ceil(w/64) u64 words per packed row (bitmap.py:35)
   int64_t bit_off;      // u64 words from the image's bitmap arena base, 32-word aligned

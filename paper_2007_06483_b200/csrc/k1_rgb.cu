@@ -1,0 +1,410 @@
+// K1 (fast path): RGB8 -> gray -> 2x box pyramid (levels 0..5) -> per-level
+// 256-bin histograms, one streaming pass over the RGB input.
+//
+// Reference semantics are those listed in pyramid.cu (image.py:58-68,
+// pyramid.py:17-62, threshold.py:25-28).  This kernel is the roofline kernel
+// of the whole path: it reads every RGB byte exactly once.  Design (sm_100a):
+//
+//  * One 1024-thread CTA per SM, persistent over a contiguous band of the
+//    interior 32x128-pixel tiles of one image (edge tiles go to the generic
+//    kernel in pyramid.cu).  Eight independent 128-thread groups each own one
+//    tile at a time and synchronise only on their own named barrier.
+//  * Each thread owns a 32-pixel row segment (96 RGB bytes).  The bytes of its
+//    NEXT tile are fetched with cp.async (LDGSTS, 16 B each, L2 evict-first
+//    policy) into the thread's own shared-memory slot right after it has
+//    pulled the current ones into registers, so the copy has a whole tile of
+//    work to land and no register holds in-flight data (32 warps/SM fit).
+//  * Gray via IDP.4A: pixel groups of 4 (12 bytes = 3 words) need 6 dp4a and
+//    3 byte-permutes; no byte extraction.
+//  * Levels 1-2 by all threads with SIMD pair sums in 16-bit lanes;
+//    levels 3-5 by one warp per tile (rotating) with warp syncs only.
+//  * Histograms: shared-memory atomics (ATOMS.POPC.INC aggregates equal
+//    addresses in a warp), reduced across a thread-block cluster through
+//    distributed shared memory, then one global RED per nonzero bin per
+//    cluster into a 128-B-strided ("spread") histogram.
+//  * Gray levels are stored with an L2::evict_last policy: the threshold pass
+//    re-reads them right after, ideally from L2.
+#include <cooperative_groups.h>
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
+#include "common.cuh"
+
+namespace cg = cooperative_groups;
+
+namespace mtb {
+
+constexpr int kK1Groups = 8;
+constexpr int kK1GroupThreads = 128;
+constexpr int kK1Threads = kK1Groups * kK1GroupThreads;
+constexpr int kHistStrideK1 = 32;   // must equal kHistStride in pyramid.cu
+
+struct K1Args {
+  const uint8_t* rgb;
+  int64_t rgb_pitch, rgb_img_stride;
+  int w, h;
+  uint8_t* gray;
+  int64_t gray_img_stride;
+  int64_t off[6], pitch[6];
+  int lw[6], lh[6];
+  int nl;                 // levels produced (1..6)
+  uint32_t* hist;         // spread histograms [img][level][bin * 32]
+  int64_t hist_img_stride;
+  int tiles_x, tiles_y;   // interior (full) tiles only: w/128 x h/32
+  int cluster;            // CTAs per cluster (1, 2, 4)
+};
+
+constexpr int kTileRgbBytes = 32 * 384;   // one 32x128 tile of RGB8
+
+struct alignas(128) GroupSmem {
+  uint8_t rgb[2][kTileRgbBytes];  // TMA ring: two tiles in flight per group
+  uint8_t l3[2][4 * 16];          // level-3 values, double-buffered by tile parity
+  uint8_t l4[2 * 8];
+  unsigned long long full[2];     // mbarriers of the two ring stages
+};
+
+struct K1Smem {
+  GroupSmem grp[kK1Groups];
+  uint32_t hist[6 * 256];
+};
+
+__device__ __forceinline__ uint32_t smem_addr(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mbar_init(unsigned long long* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_addr(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(unsigned long long* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_addr(bar)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(unsigned long long* bar, uint32_t parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      "@!p bra WAIT_%=;\n"
+      "}\n" ::"r"(smem_addr(bar)),
+      "r"(parity)
+      : "memory");
+}
+// TMA 3-D tile copy (box 96 u32 x 32 rows x 1 image) -> this CTA's smem.
+__device__ __forceinline__ void tma_tile(void* dst, const CUtensorMap* map, int c0, int c1, int c2,
+                                         unsigned long long* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], "
+      "[%5];" ::"r"(smem_addr(dst)),
+      "l"(map), "r"(c0), "r"(c1), "r"(c2), "r"(smem_addr(bar))
+      : "memory");
+}
+// Bulk (TMA engine) copy of `bytes` contiguous bytes global -> this CTA's smem,
+// completing on `bar` (tx count).
+__device__ __forceinline__ void bulk_copy(void* dst, const void* src, uint32_t bytes, unsigned long long* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                   smem_addr(dst)),
+               "l"(src), "r"(bytes), "r"(smem_addr(bar))
+               : "memory");
+}
+
+__device__ __forceinline__ uint4 ld_stream16(const void* p) {
+  uint4 r;
+  asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+               : "l"(p));
+  return r;
+}
+__device__ __forceinline__ void group_bar(int g) {
+  asm volatile("bar.sync %0, %1;" ::"r"(g + 1), "r"(kK1GroupThreads) : "memory");
+}
+
+// Four gray values (dp4a sums, gray = byte 1) of the 4 pixels in words w0..w2
+// ([R0 G0 B0 R1] [G1 B1 R2 G2] [B2 R3 G3 B3]); returns the packed gray word.
+__device__ __forceinline__ uint32_t gray4(uint32_t w0, uint32_t w1, uint32_t w2, uint32_t (&s)[4]) {
+  s[0] = __dp4a(w0, 0x0013B736u, 0u);
+  s[1] = __dp4a(w1, 0x000013B7u, __dp4a(w0, 0x36000000u, 0u));
+  s[2] = __dp4a(w2, 0x00000013u, __dp4a(w1, 0xB7360000u, 0u));
+  s[3] = __dp4a(w2, 0x13B73600u, 0u);
+  const uint32_t g01 = __byte_perm(s[0], s[1], 0x0051);
+  const uint32_t g23 = __byte_perm(s[2], s[3], 0x0051);
+  return __byte_perm(g01, g23, 0x5410);
+}
+
+// Two 2x2 box averages from one word of each of two rows (4 source pixels
+// per word): avg of bytes 0-1 in byte 0, avg of bytes 2-3 in byte 2.
+__device__ __forceinline__ uint32_t box2(uint32_t u, uint32_t d) {
+  const uint32_t s = (u & 0x00FF00FFu) + ((u >> 8) & 0x00FF00FFu) + (d & 0x00FF00FFu) + ((d >> 8) & 0x00FF00FFu) +
+                     0x00020002u;
+  return s >> 2;
+}
+// Pack the two results of two box2 words into 4 consecutive bytes.
+__device__ __forceinline__ uint32_t pack_box(uint32_t q0, uint32_t q1) { return __byte_perm(q0, q1, 0x6420); }
+
+// Thread layout inside a 128-thread group (one 32x128 tile): thread = (ry, cx)
+// owns level-0 rows 2ry, 2ry+1 and columns 16cx .. 16cx+15 (ry 0..15, cx 0..7);
+// lane = (ry & 3) * 8 + cx, warp-in-group = ry >> 2.  Level 1 is computed in
+// registers, level 2 with one shuffle (partner ry^1 = lane^8), level 3 with
+// another (partner ry^2 = lane^16); levels 4-5 (which span warps) go through a
+// 64-byte shared buffer and one named barrier per tile.
+__global__ void __launch_bounds__(kK1Threads, 1) k1_rgb_pyramid_kernel(K1Args a, const __grid_constant__ CUtensorMap rgb_map) {
+  extern __shared__ __align__(128) uint8_t k1_smem_raw[];
+  K1Smem& SM = *reinterpret_cast<K1Smem*>(k1_smem_raw);
+  uint32_t* s_hist = SM.hist;
+
+  const int tid = threadIdx.x;
+  const int g = tid >> 7;             // group
+  const int t = tid & 127;            // thread in group
+  const int lane = tid & 31;
+  const int wig = t >> 5;             // warp in group
+  const int cx = lane & 7;
+  const int ry = (wig << 2) | (lane >> 3);
+  const int img = blockIdx.y;
+  GroupSmem& S = SM.grp[g];
+
+  for (int i = tid; i < 6 * 256; i += kK1Threads) s_hist[i] = 0;
+  if (t == 0) {
+    mbar_init(&S.full[0], 1);
+    mbar_init(&S.full[1], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+
+  const uint8_t* rgb = a.rgb + img * a.rgb_img_stride;
+  uint8_t* gray = a.gray + img * a.gray_img_stride;
+
+  const int ntiles = a.tiles_x * a.tiles_y;
+  const int t_begin = (int)((int64_t)blockIdx.x * ntiles / gridDim.x);
+  const int t_end = (int)((int64_t)(blockIdx.x + 1) * ntiles / gridDim.x);
+
+  // One thread per group streams tiles into the group's 2-stage ring with a
+  // single TMA tensor copy each (box = the tile's 32 rows x 384 bytes).
+  auto issue = [&](int tile, int stage) {
+    if (t == 0) {
+      const int ty = tile / a.tiles_x, tx = tile - ty * a.tiles_x;
+      mbar_expect_tx(&S.full[stage], kTileRgbBytes);
+      tma_tile(S.rgb[stage], &rgb_map, 96 * tx, 32 * ty, img, &S.full[stage]);
+    }
+  };
+  if (t_begin + g < t_end) issue(t_begin + g, 0);
+  if (t_begin + g + kK1Groups < t_end) issue(t_begin + g + kK1Groups, 1);
+
+  int iter = 0;
+  for (int tile = t_begin + g; tile < t_end; tile += kK1Groups, ++iter) {
+    const int ty = tile / a.tiles_x, tx = tile - ty * a.tiles_x;
+    const int y0 = ty * 32 + 2 * ry, x0 = tx * 128 + 16 * cx;
+    const int stage = iter & 1;
+
+    // ---- level 0: 2 rows x 16 pixels --------------------------------------
+    uint32_t gw[2][4];
+    {
+      mbar_wait(&S.full[stage], (iter >> 1) & 1);
+      const uint8_t* p0 = S.rgb[stage] + (2 * ry) * 384 + 48 * cx;
+      const uint8_t* p1 = p0 + 384;
+      const uint4 q0 = *reinterpret_cast<const uint4*>(p0), q1 = *reinterpret_cast<const uint4*>(p0 + 16),
+                  q2 = *reinterpret_cast<const uint4*>(p0 + 32);
+      const uint4 q3 = *reinterpret_cast<const uint4*>(p1), q4 = *reinterpret_cast<const uint4*>(p1 + 16),
+                  q5 = *reinterpret_cast<const uint4*>(p1 + 32);
+      const uint32_t wv[2][12] = {{q0.x, q0.y, q0.z, q0.w, q1.x, q1.y, q1.z, q1.w, q2.x, q2.y, q2.z, q2.w},
+                                  {q3.x, q3.y, q3.z, q3.w, q4.x, q4.y, q4.z, q4.w, q5.x, q5.y, q5.z, q5.w}};
+#pragma unroll
+      for (int j = 0; j < 2; ++j) {
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          uint32_t s4[4];
+          gw[j][k] = gray4(wv[j][3 * k], wv[j][3 * k + 1], wv[j][3 * k + 2], s4);
+#pragma unroll
+          for (int i = 0; i < 4; ++i) atomicAdd(&s_hist[s4[i] >> 8], 1u);
+        }
+        *reinterpret_cast<uint4*>(gray + a.off[0] + (int64_t)(y0 + j) * a.pitch[0] + x0) =
+            make_uint4(gw[j][0], gw[j][1], gw[j][2], gw[j][3]);
+      }
+    }
+    if (a.nl >= 2) {
+    // ---- level 1: 1 row x 8 pixels, in registers --------------------------
+    uint32_t l1[2];
+    {
+      l1[0] = pack_box(box2(gw[0][0], gw[1][0]), box2(gw[0][1], gw[1][1]));
+      l1[1] = pack_box(box2(gw[0][2], gw[1][2]), box2(gw[0][3], gw[1][3]));
+      *reinterpret_cast<uint2*>(gray + a.off[1] + (int64_t)(ty * 16 + ry) * a.pitch[1] + tx * 64 + 8 * cx) =
+          make_uint2(l1[0], l1[1]);
+#pragma unroll
+      for (int i = 0; i < 8; ++i) atomicAdd(&s_hist[256 + ((l1[i >> 2] >> (8 * (i & 3))) & 0xff)], 1u);
+    }
+    if (a.nl >= 3) {
+    // ---- level 2: partner ry^1 (lane^8); even-ry thread emits 4 pixels ----
+    uint32_t l2 = 0;
+    {
+      const uint32_t o0 = __shfl_xor_sync(0xffffffffu, l1[0], 8);
+      const uint32_t o1 = __shfl_xor_sync(0xffffffffu, l1[1], 8);
+      if ((ry & 1) == 0) {
+        l2 = pack_box(box2(l1[0], o0), box2(l1[1], o1));
+        *reinterpret_cast<uint32_t*>(gray + a.off[2] + (int64_t)(ty * 8 + (ry >> 1)) * a.pitch[2] + tx * 32 +
+                                     4 * cx) = l2;
+#pragma unroll
+        for (int i = 0; i < 4; ++i) atomicAdd(&s_hist[512 + ((l2 >> (8 * i)) & 0xff)], 1u);
+      }
+    }
+    if (a.nl >= 4) {
+    // ---- level 3: partner ry^2 (lane^16); ry%4==0 thread emits 2 pixels ---
+    {
+      const uint32_t o = __shfl_xor_sync(0xffffffffu, l2, 16);
+      if ((ry & 3) == 0) {
+        const uint32_t q = box2(l2, o);
+        const uint32_t v0 = q & 0xff, v1 = (q >> 16) & 0xff;
+        const uint16_t pk = (uint16_t)(v0 | (v1 << 8));
+        const int r3 = ry >> 2;  // 0..3
+        *reinterpret_cast<uint16_t*>(&S.l3[iter & 1][r3 * 16 + 2 * cx]) = pk;
+        *reinterpret_cast<uint16_t*>(gray + a.off[3] + (int64_t)(ty * 4 + r3) * a.pitch[3] + tx * 16 + 2 * cx) =
+            pk;
+        atomicAdd(&s_hist[768 + v0], 1u);
+        atomicAdd(&s_hist[768 + v1], 1u);
+      }
+    }
+    }}}
+    group_bar(g);  // every thread has consumed ring stage `stage` (and written l3)
+    if (tile + 2 * kK1Groups < t_end) {
+      if (t == 0) asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      issue(tile + 2 * kK1Groups, stage);
+    }
+    if (a.nl < 5) continue;
+
+    // ---- levels 4..5: one warp of the group (rotating) --------------------
+    if (wig == (iter & 3)) {
+      const uint8_t* l3 = S.l3[iter & 1];
+      if (lane < 16) {  // level 4: 2 x 8
+        const int r = lane >> 3, c = lane & 7;
+        const uint8_t* sp = l3 + (2 * r) * 16 + 2 * c;
+        const uint32_t v = (sp[0] + sp[1] + sp[16] + sp[17] + 2u) >> 2;
+        S.l4[r * 8 + c] = (uint8_t)v;
+        gray[a.off[4] + (int64_t)(ty * 2 + r) * a.pitch[4] + tx * 8 + c] = (uint8_t)v;
+        atomicAdd(&s_hist[1024 + v], 1u);
+      }
+      __syncwarp();
+      if (a.nl > 5 && lane < 4) {  // level 5: 1 x 4
+        const uint8_t* sp = S.l4 + 2 * lane;
+        const uint32_t v = (sp[0] + sp[1] + sp[8] + sp[9] + 2u) >> 2;
+        gray[a.off[5] + (int64_t)ty * a.pitch[5] + tx * 4 + lane] = (uint8_t)v;
+        atomicAdd(&s_hist[1280 + v], 1u);
+      }
+      __syncwarp();
+    }
+  }
+
+  // ---- histogram reduction: CTA -> cluster leader (DSMEM) -> global -------
+  __syncthreads();
+  uint32_t* gh = a.hist + img * a.hist_img_stride;
+  const int nbins = a.nl * 256;
+  if (a.cluster > 1) {
+    cg::cluster_group cl = cg::this_cluster();
+    cl.sync();
+    if (cl.block_rank() != 0) {
+      uint32_t* dst = cl.map_shared_rank(s_hist, 0);
+      for (int i = tid; i < nbins; i += kK1Threads) {
+        const uint32_t v = s_hist[i];
+        if (v) atomicAdd(&dst[i], v);
+      }
+    }
+    cl.sync();
+    if (cl.block_rank() != 0) return;
+  }
+  for (int i = tid; i < nbins; i += kK1Threads) {
+    const uint32_t v = s_hist[i];
+    if (v) atomicAdd(&gh[(int64_t)i * kHistStrideK1], v);
+  }
+}
+
+static PFN_cuTensorMapEncodeTiled_v12000 encode_tiled() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  if (!fn) {
+    cudaDriverEntryPointQueryResult q;
+    void* p = nullptr;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  }
+  return fn;
+}
+
+bool k1_rgb_supported(int w, int64_t rgb_pitch, int64_t rgb_img_stride, const void* rgb) {
+  return (3 * (int64_t)w) % 4 == 0 && (rgb_pitch & 15) == 0 && (rgb_img_stride & 15) == 0 &&
+         ((uintptr_t)rgb & 15) == 0 && encode_tiled() != nullptr;
+}
+
+// Levels 0..min(n,6)-1 of the interior tiles of n_img images (chunks of <= 4
+// images per launch so every launch fills the GPU with one CTA per SM).
+int launch_k1_rgb(const uint8_t* rgb, int64_t rgb_pitch, int64_t rgb_img_stride, int n_img, const Plan& p,
+                  uint8_t* gray, uint32_t* spread_hist, int64_t hist_img_stride, cudaStream_t st) {
+  K1Args a{};
+  a.rgb_pitch = rgb_pitch;
+  a.rgb_img_stride = rgb_img_stride;
+  a.w = p.lv[0].w;
+  a.h = p.lv[0].h;
+  a.gray_img_stride = p.gray_img_bytes;
+  a.nl = p.n < 6 ? p.n : 6;
+  for (int k = 0; k < 6; ++k) {
+    const int l = k < p.n ? k : p.n - 1;
+    a.off[k] = p.lv[l].gray_off;
+    a.pitch[k] = p.lv[l].gray_pitch;
+    a.lw[k] = k < p.n ? p.lv[k].w : 0;
+    a.lh[k] = k < p.n ? p.lv[k].h : 0;
+  }
+  a.hist_img_stride = hist_img_stride;
+  a.tiles_x = a.w / 128;   // interior tiles; edge tiles go to the generic kernel
+  a.tiles_y = a.h / 32;
+  const int ntiles = a.tiles_x * a.tiles_y;
+  if (ntiles == 0) return MTB_OK;
+  static bool attr_done = false;
+  const int smem = (int)sizeof(K1Smem);
+  if (!attr_done) {
+    MTB_CUDA(cudaFuncSetAttribute(k1_rgb_pyramid_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    attr_done = true;
+  }
+  const int sms = num_sms();
+  int launches = 0;
+  for (int i0 = 0; i0 < n_img; i0 += 4) {
+    const int c = n_img - i0 < 4 ? n_img - i0 : 4;
+    int x = sms / c;
+    if (x > (ntiles + kK1Groups - 1) / kK1Groups) x = (ntiles + kK1Groups - 1) / kK1Groups;
+    if (x < 1) x = 1;
+    int cl = 1;
+    if (x % 4 == 0) cl = 4;
+    else if (x % 2 == 0) cl = 2;
+    a.cluster = cl;
+    a.rgb = rgb + i0 * rgb_img_stride;
+    a.gray = gray + i0 * p.gray_img_bytes;
+    CUtensorMap map;
+    {
+      const cuuint64_t dims[3] = {(cuuint64_t)(3 * (int64_t)a.w / 4), (cuuint64_t)a.h, (cuuint64_t)c};
+      const cuuint64_t strides[2] = {(cuuint64_t)rgb_pitch, (cuuint64_t)rgb_img_stride};
+      const cuuint32_t box[3] = {96, 32, 1};
+      const cuuint32_t estr[3] = {1, 1, 1};
+      const CUresult r = encode_tiled()(&map, CU_TENSOR_MAP_DATA_TYPE_UINT32, 3, (void*)a.rgb, dims, strides, box,
+                                        estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                                        CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+      if (r != CUDA_SUCCESS) {
+        set_error("cuTensorMapEncodeTiled failed for the RGB batch");
+        return MTB_ECUDA;
+      }
+    }
+    a.hist = spread_hist + i0 * hist_img_stride;
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3((unsigned)x, (unsigned)c);
+    cfg.blockDim = dim3(kK1Threads);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = cl;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    const cudaError_t e = cudaLaunchKernelEx(&cfg, k1_rgb_pyramid_kernel, a, map);
+    if (e != cudaSuccess) {
+      set_error(std::string("k1_rgb_pyramid_kernel: ") + cudaGetErrorString(e));
+      return MTB_ECUDA;
+    }
+    ++launches;
+  }
+  return check_launch("k1_rgb_pyramid_kernel", launches);
+}
+
+}  // namespace mtb

@@ -40,6 +40,7 @@ struct PyrArgs {
   int64_t hist_img_stride;            // u32 elements
   int hist_level0;                    // global level index of t = 0
   int tiles_x, tiles_y;
+  int edge_only;                      // 1: only the partial right column / bottom row tiles
 };
 
 __device__ __forceinline__ uint4 ld_stream16(const void* p) {
@@ -86,8 +87,24 @@ pyramid_tiles_kernel(PyrArgs a) {
   const int ntiles = a.tiles_x * a.tiles_y;
   __syncthreads();
 
-  for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-    const int ty = tile / a.tiles_x, tx = tile - ty * a.tiles_x;
+  // Edge mode: tiles of the partial right column (if w % 128) then of the
+  // partial bottom row (if h % 32), the ones the interior kernel skips.
+  const bool col_part = (a.src_w % kTileCols) != 0, row_part = (a.src_h % kTileRows) != 0;
+  const int n_col = col_part ? a.tiles_y : 0;
+  const int n_row = row_part ? a.tiles_x - (col_part ? 1 : 0) : 0;
+  const int n_work = a.edge_only ? n_col + n_row : ntiles;
+  for (int tile = blockIdx.x; tile < n_work; tile += gridDim.x) {
+    int ty, tx;
+    if (!a.edge_only) {
+      ty = tile / a.tiles_x;
+      tx = tile - ty * a.tiles_x;
+    } else if (tile < n_col) {
+      ty = tile;
+      tx = a.tiles_x - 1;
+    } else {
+      ty = a.tiles_y - 1;
+      tx = tile - n_col;
+    }
 
     // ---- level s (t = 0): 16 pixels per thread -------------------------
     {
@@ -334,16 +351,63 @@ int64_t spread_hist_elems(int n_levels) { return (int64_t)n_levels * 256 * kHist
 
 // Builds gray levels 0..n-1 (plan p) and their spread histograms for n_img
 // images.  Level 0 comes from RGB; deeper levels are produced 6 per pass.
+int launch_k1_rgb(const uint8_t* rgb, int64_t rgb_pitch, int64_t rgb_img_stride, int n_img, const Plan& p,
+                  uint8_t* gray, uint32_t* spread_hist, int64_t hist_img_stride, cudaStream_t st);
+bool k1_rgb_supported(int w, int64_t rgb_pitch, int64_t rgb_img_stride, const void* rgb);
+
+// Builds gray levels 0..n-1 (plan p) and their spread histograms for n_img
+// images: levels 0..5 by the fused RGB kernel (k1_rgb.cu), deeper levels by
+// tile passes over the deepest level produced so far (6 levels per pass).
 int launch_pyramid(const uint8_t* rgb, int64_t rgb_pitch, int64_t rgb_img_stride, int n_img,
                    const Plan& p, uint8_t* gray, uint32_t* spread_hist, cudaStream_t st) {
-  int s = 0;
+  // Interior tiles: the fast kernel (needs 16-B aligned RGB rows).  Edge
+  // tiles (and every tile when rows are unaligned): the generic kernel.
+  const bool vec_ok = k1_rgb_supported(p.lv[0].w, rgb_pitch, rgb_img_stride, rgb);
   int launches = 0;
-  while (s < p.n) {
+  if (vec_ok) {
+    int rc = launch_k1_rgb(rgb, rgb_pitch, rgb_img_stride, n_img, p, gray, spread_hist, spread_hist_elems(p.n), st);
+    if (rc) return rc;
+  }
+  {
     PyrArgs a{};
-    const bool from_rgb = (s == 0);
-    a.src = from_rgb ? rgb : gray + p.lv[s].gray_off;
-    a.src_pitch = from_rgb ? rgb_pitch : p.lv[s].gray_pitch;
-    a.src_img_stride = from_rgb ? rgb_img_stride : p.gray_img_bytes;
+    a.src = rgb;
+    a.src_pitch = rgb_pitch;
+    a.src_img_stride = rgb_img_stride;
+    a.src_w = p.lv[0].w;
+    a.src_h = p.lv[0].h;
+    a.gray = gray;
+    a.gray_img_stride = p.gray_img_bytes;
+    a.nl = p.n < kTileLevels ? p.n : kTileLevels;
+    for (int t = 0; t < kTileLevels; ++t) {
+      const int l = t < p.n ? t : p.n - 1;
+      a.off[t] = p.lv[l].gray_off;
+      a.pitch[t] = t < p.n ? p.lv[l].gray_pitch : 0;
+      a.w[t] = t < p.n ? p.lv[l].w : 0;
+      a.h[t] = t < p.n ? p.lv[l].h : 0;
+    }
+    a.hist = spread_hist;
+    a.hist_img_stride = spread_hist_elems(p.n);
+    a.hist_level0 = 0;
+    a.tiles_x = (int)((a.src_w + kTileCols - 1) / kTileCols);
+    a.tiles_y = (int)((a.src_h + kTileRows - 1) / kTileRows);
+    a.edge_only = vec_ok ? 1 : 0;
+    const int64_t n_edge = ((a.src_w % kTileCols) ? a.tiles_y : 0) +
+                           ((a.src_h % kTileRows) ? a.tiles_x - ((a.src_w % kTileCols) ? 1 : 0) : 0);
+    const int64_t ntiles = vec_ok ? n_edge : (int64_t)a.tiles_x * a.tiles_y;
+    if (ntiles > 0) {
+      int64_t per_img = (int64_t)num_sms() * 4 / (n_img > 0 ? n_img : 1);
+      if (per_img < 1) per_img = 1;
+      if (per_img > ntiles) per_img = ntiles;
+      pyramid_tiles_kernel<true><<<dim3((unsigned)per_img, (unsigned)n_img), kPyrThreads, 0, st>>>(a);
+      ++launches;
+    }
+  }
+  int s = 5;
+  while (s < p.n - 1) {
+    PyrArgs a{};
+    a.src = gray + p.lv[s].gray_off;
+    a.src_pitch = p.lv[s].gray_pitch;
+    a.src_img_stride = p.gray_img_bytes;
     a.src_w = p.lv[s].w;
     a.src_h = p.lv[s].h;
     a.gray = gray;
@@ -361,22 +425,16 @@ int launch_pyramid(const uint8_t* rgb, int64_t rgb_pitch, int64_t rgb_img_stride
     a.hist_level0 = s;
     a.tiles_x = (int)((a.src_w + kTileCols - 1) / kTileCols);
     a.tiles_y = (int)((a.src_h + kTileRows - 1) / kTileRows);
+    a.edge_only = 0;
     const int64_t ntiles = (int64_t)a.tiles_x * a.tiles_y;
     int64_t per_img = (int64_t)num_sms() * 4 / (n_img > 0 ? n_img : 1);
     if (per_img < 1) per_img = 1;
     if (per_img > ntiles) per_img = ntiles;
-    dim3 grid((unsigned)per_img, (unsigned)n_img);
-    if (from_rgb)
-      pyramid_tiles_kernel<true><<<grid, kPyrThreads, 0, st>>>(a);
-    else
-      pyramid_tiles_kernel<false><<<grid, kPyrThreads, 0, st>>>(a);
+    pyramid_tiles_kernel<false><<<dim3((unsigned)per_img, (unsigned)n_img), kPyrThreads, 0, st>>>(a);
     ++launches;
-    // Next pass starts from the deepest level this pass produced.
-    const int produced = s + a.nl - 1;
-    if (produced >= p.n - 1) break;
-    s = produced;
+    s += a.nl - 1;
   }
-  return check_launch("pyramid_tiles_kernel", launches);
+  return launches ? check_launch("pyramid_tiles_kernel", launches) : MTB_OK;
 }
 
 int launch_hist_median(const uint32_t* spread_hist, int n_img, int n_levels, uint32_t* dense,

@@ -94,8 +94,22 @@ __global__ void select_candidate_kernel(const unsigned long long* errs, const in
 }
 
 // ----------------------------------------------------------- level search --
-constexpr int kSearchWarps = 4;
-constexpr int kSearchRows = 8;   // rows per warp strip
+// One CTA = one tile of 64 output rows x 32 words (1024 pixels) of one pair's
+// level.  The reference maps A/EA of the tile and the target maps B/EB of the
+// tile plus its halo (rows -1..+1 around the base dy, words -2..+1 around the
+// base dx) are staged in shared memory with coalesced loads issued all at
+// once; then each warp slides down 8 output rows keeping the three source
+// rows it needs, each pre-shifted by bx-1, bx, bx+1 (funnel shifts), in
+// registers.  Per output word: 9 x (2 LOP3 + POPC).  CTA partials go to the
+// pair's 9 u64 counters; the last CTA of the pair picks the winner with the
+// search.py:67 key and publishes it for the next level.
+constexpr int kSTRows = 64;          // output rows per tile
+constexpr int kSTWords = 32;         // output words per tile
+constexpr int kSTWarps = 8;          // 8 rows per warp
+constexpr int kSTThreads = kSTWarps * 32;
+constexpr int kSTBRows = kSTRows + 2;
+constexpr int kSTBWords = kSTWords + 3;
+constexpr int kSTBPitch = kSTBWords + 1;
 
 struct LevelSearchArgs {
   const uint64_t* const* maps;   // [P][4] {ref.mtb, ref.excl, tgt.mtb, tgt.excl}
@@ -109,48 +123,25 @@ struct LevelSearchArgs {
   int64_t errs_stride;
   uint32_t* done;
   int64_t done_stride;
-  int chunks;                    // ceil(nw32 / 32)
+  int tiles_x;                   // ceil(nw32 / 32)
 };
 
-struct ShiftedRow {
-  uint32_t b[3], e[3];           // row shifted by bx-1, bx, bx+1
+struct SearchSmem {
+  uint32_t a[kSTRows][kSTWords];
+  uint32_t ea[kSTRows][kSTWords];
+  uint32_t b[kSTBRows][kSTBPitch];
+  uint32_t eb[kSTBRows][kSTBPitch];
+  unsigned part[kSTWarps][9];
+  int last;
 };
 
-__device__ __forceinline__ ShiftedRow load_shifted(const uint32_t* bm, const uint32_t* em, int64_t sy, int h,
-                                                   int nw32, int64_t j, int qb, const int (&o)[3],
-                                                   const int (&r)[3]) {
-  ShiftedRow s;
-  uint32_t wb[4] = {0, 0, 0, 0}, we[4] = {0, 0, 0, 0};
-  if (sy >= 0 && sy < h && j < nw32) {
-    const uint32_t* br = bm + sy * nw32;
-    const uint32_t* er = em + sy * nw32;
-#pragma unroll
-    for (int i = 0; i < 4; ++i) {
-      const int64_t idx = j - qb - 2 + i;  // W[j-qb-2 .. j-qb+1]
-      wb[i] = row_word(br, idx, nw32);
-      we[i] = row_word(er, idx, nw32);
-    }
-  }
-#pragma unroll
-  for (int d = 0; d < 3; ++d) {
-    // W[j-q] = w[2-o], W[j-q-1] = w[1-o] with o = q - qb in {-1, 0, 1}
-    const uint32_t hb = o[d] < 0 ? wb[3] : (o[d] == 0 ? wb[2] : wb[1]);
-    const uint32_t lb = o[d] < 0 ? wb[2] : (o[d] == 0 ? wb[1] : wb[0]);
-    const uint32_t he = o[d] < 0 ? we[3] : (o[d] == 0 ? we[2] : we[1]);
-    const uint32_t le = o[d] < 0 ? we[2] : (o[d] == 0 ? we[1] : we[0]);
-    s.b[d] = shifted_word(lb, hb, r[d]);
-    s.e[d] = shifted_word(le, he, r[d]);
-  }
-  return s;
-}
-
-__global__ void __launch_bounds__(kSearchWarps * 32)
+__global__ void __launch_bounds__(kSTThreads)
 level_search_kernel(LevelSearchArgs a) {
-  __shared__ unsigned s_part[kSearchWarps][9];
-  __shared__ int s_last;
+  __shared__ SearchSmem S;
   const int p = blockIdx.y;
-  const int lane = threadIdx.x & 31, wi = threadIdx.x >> 5;
-  const int chunk = blockIdx.x % a.chunks, group = blockIdx.x / a.chunks;
+  const int tid = threadIdx.x, lane = tid & 31, wi = tid >> 5;
+  const int tx = blockIdx.x % a.tiles_x, ty = blockIdx.x / a.tiles_x;
+  const int y0 = ty * kSTRows, j0 = tx * kSTWords;
   const uint32_t* A = reinterpret_cast<const uint32_t*>(a.maps[4 * p + 0]);
   const uint32_t* EA = reinterpret_cast<const uint32_t*>(a.maps[4 * p + 1]);
   const uint32_t* B = reinterpret_cast<const uint32_t*>(a.maps[4 * p + 2]);
@@ -165,58 +156,99 @@ level_search_kernel(LevelSearchArgs a) {
     by = a.base[2 * p + 1];
   }
   const int qb = bx >> 5;
+  const int sy0 = y0 - by - 1;           // first staged source row
+  const int64_t sj0 = (int64_t)j0 - qb - 2;  // first staged source word
+
+  // ---- stage (all loads in flight together) ----
+  for (int i = tid; i < kSTRows * kSTWords; i += kSTThreads) {
+    const int r = i / kSTWords, c = i - r * kSTWords;
+    const int y = y0 + r, j = j0 + c;
+    const bool ok = y < a.h && j < a.nw32;
+    S.a[r][c] = ok ? __ldg(A + (int64_t)y * a.nw32 + j) : 0u;
+    S.ea[r][c] = ok ? __ldg(EA + (int64_t)y * a.nw32 + j) : 0u;
+  }
+  for (int i = tid; i < kSTBRows * kSTBWords; i += kSTThreads) {
+    const int r = i / kSTBWords, c = i - r * kSTBWords;
+    const int64_t y = (int64_t)sy0 + r, j = sj0 + c;
+    const bool ok = y >= 0 && y < a.h && j >= 0 && j < a.nw32;
+    S.b[r][c] = ok ? __ldg(B + y * a.nw32 + j) : 0u;
+    S.eb[r][c] = ok ? __ldg(EB + y * a.nw32 + j) : 0u;
+  }
+  __syncthreads();
+
+  // ---- compute: warp wi -> output rows 8wi .. 8wi+7, lane -> word ----
   int o[3], r[3];
 #pragma unroll
   for (int d = 0; d < 3; ++d) {
     const int dx = bx + d - 1;
-    o[d] = (dx >> 5) - qb;
+    o[d] = (dx >> 5) - qb;  // in {-1, 0, 1}
     r[d] = dx & 31;
   }
-
-  const int64_t j = (int64_t)chunk * 32 + lane;
-  const int y0 = (group * kSearchWarps + wi) * kSearchRows;
+  // Source row lb (local) shifted by bx-1, bx, bx+1: W[j-q] = w[2-o], W[j-q-1] = w[1-o]
+  // with w[i] = staged word lane + i.
+  auto shifted_row = [&](int lb, uint32_t (&sb)[3], uint32_t (&se)[3]) {
+    uint32_t wb[4], we[4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      wb[i] = S.b[lb][lane + i];
+      we[i] = S.eb[lb][lane + i];
+    }
+#pragma unroll
+    for (int d = 0; d < 3; ++d) {
+      const uint32_t hb = o[d] < 0 ? wb[3] : (o[d] == 0 ? wb[2] : wb[1]);
+      const uint32_t lb_ = o[d] < 0 ? wb[2] : (o[d] == 0 ? wb[1] : wb[0]);
+      const uint32_t he = o[d] < 0 ? we[3] : (o[d] == 0 ? we[2] : we[1]);
+      const uint32_t le = o[d] < 0 ? we[2] : (o[d] == 0 ? we[1] : we[0]);
+      sb[d] = shifted_word(lb_, hb, r[d]);
+      se[d] = shifted_word(le, he, r[d]);
+    }
+  };
   unsigned cnt[9];
 #pragma unroll
   for (int i = 0; i < 9; ++i) cnt[i] = 0;
-
-  if (y0 < a.h) {
-    // Window of source rows y-by-1 (ddy=+1), y-by (ddy=0), y-by+1 (ddy=-1).
-    ShiftedRow w0 = load_shifted(B, EB, (int64_t)y0 - by - 1, a.h, a.nw32, j, qb, o, r);
-    ShiftedRow w1 = load_shifted(B, EB, (int64_t)y0 - by, a.h, a.nw32, j, qb, o, r);
-    for (int y = y0; y < y0 + kSearchRows && y < a.h; ++y) {
-      const ShiftedRow w2 = load_shifted(B, EB, (int64_t)y - by + 1, a.h, a.nw32, j, qb, o, r);
-      if (j < a.nw32) {
-        const uint32_t av = __ldg(A + (int64_t)y * a.nw32 + j);
-        const uint32_t ev = __ldg(EA + (int64_t)y * a.nw32 + j);
+  const int rbeg = wi * (kSTRows / kSTWarps);
+  if (y0 + rbeg < a.h) {
+    // output local row rr needs source local rows rr (ddy=+1), rr+1 (ddy=0), rr+2 (ddy=-1)
+    uint32_t b0[3], e0[3], b1[3], e1[3];
+    shifted_row(rbeg, b0, e0);
+    shifted_row(rbeg + 1, b1, e1);
 #pragma unroll
-        for (int d = 0; d < 3; ++d) {
-          cnt[0 + d] += __popc((av ^ w2.b[d]) & ev & w2.e[d]);  // ddy = -1
-          cnt[3 + d] += __popc((av ^ w1.b[d]) & ev & w1.e[d]);  // ddy =  0
-          cnt[6 + d] += __popc((av ^ w0.b[d]) & ev & w0.e[d]);  // ddy = +1
-        }
+    for (int k = 0; k < kSTRows / kSTWarps; ++k) {
+      const int rr = rbeg + k;
+      uint32_t b2[3], e2[3];
+      shifted_row(rr + 2, b2, e2);
+      const uint32_t av = S.a[rr][lane], ev = S.ea[rr][lane];
+#pragma unroll
+      for (int d = 0; d < 3; ++d) {
+        cnt[0 + d] += __popc((av ^ b2[d]) & ev & e2[d]);  // ddy = -1
+        cnt[3 + d] += __popc((av ^ b1[d]) & ev & e1[d]);  // ddy =  0
+        cnt[6 + d] += __popc((av ^ b0[d]) & ev & e0[d]);  // ddy = +1
       }
-      w0 = w1;
-      w1 = w2;
+#pragma unroll
+      for (int d = 0; d < 3; ++d) {
+        b0[d] = b1[d]; e0[d] = e1[d];
+        b1[d] = b2[d]; e1[d] = e2[d];
+      }
     }
   }
 #pragma unroll
   for (int i = 0; i < 9; ++i) {
     const unsigned v = warp_sum(cnt[i]);
-    if (lane == 0) s_part[wi][i] = v;
+    if (lane == 0) S.part[wi][i] = v;
   }
   __syncthreads();
   unsigned long long* errs = a.errs + p * a.errs_stride;
-  if (threadIdx.x < 9) {
+  if (tid < 9) {
     unsigned long long v = 0;
 #pragma unroll
-    for (int k = 0; k < kSearchWarps; ++k) v += s_part[k][threadIdx.x];
-    if (v) atomicAdd(&errs[threadIdx.x], v);
+    for (int k = 0; k < kSTWarps; ++k) v += S.part[k][tid];
+    if (v) atomicAdd(&errs[tid], v);
   }
   __threadfence();
   __syncthreads();
-  if (threadIdx.x == 0) s_last = (atomicAdd(&a.done[p * a.done_stride], 1u) == gridDim.x - 1);
+  if (tid == 0) S.last = (atomicAdd(&a.done[p * a.done_stride], 1u) == gridDim.x - 1);
   __syncthreads();
-  if (s_last && threadIdx.x == 0) {
+  if (S.last && tid == 0) {
     __threadfence();
     int best = 0;
     unsigned long long be = 0;
@@ -224,8 +256,7 @@ level_search_kernel(LevelSearchArgs a) {
 #pragma unroll
     for (int i = 0; i < 9; ++i) {
       const unsigned long long e = *((volatile unsigned long long*)&errs[i]);
-      const int ddy = i / 3 - 1, ddx = i % 3 - 1;
-      const int d = abs(ddx) + abs(ddy);
+      const int d = abs(i % 3 - 1) + abs(i / 3 - 1);
       if (i == 0 || key_less(e, d, i, be, bd, best)) { best = i; be = e; bd = d; }
     }
     a.acc[p * a.acc_stride] = bx + best % 3 - 1;
@@ -333,10 +364,9 @@ extern "C" int mtb_find_offset_batch(const uint64_t* const* maps, const int32_t*
     a.errs_stride = 9 * n_levels;
     a.done = done + k;
     a.done_stride = n_levels;
-    a.chunks = (a.nw32 + 31) / 32;
-    const int rows_per_cta = kSearchWarps * kSearchRows;
-    const int groups = (a.h + rows_per_cta - 1) / rows_per_cta;
-    level_search_kernel<<<dim3(a.chunks * groups, P), kSearchWarps * 32, 0, st>>>(a);
+    a.tiles_x = (a.nw32 + kSTWords - 1) / kSTWords;
+    const int tiles_y = (a.h + kSTRows - 1) / kSTRows;
+    level_search_kernel<<<dim3(a.tiles_x * tiles_y, P), kSTThreads, 0, st>>>(a);
     ++launches;
   }
   return check_launch("level_search_kernel", launches);

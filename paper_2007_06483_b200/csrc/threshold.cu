@@ -15,10 +15,11 @@ namespace mtb {
 
 struct ThreshLevel {
   int w, h;
-  int64_t gray_off, gray_pitch;  // bytes
+  int64_t gray_off, gray_pitch;  // bytes (pitch is a multiple of 128)
   int64_t bit_off;               // u64 words
   int nw32;                      // u32 words per packed row
-  int64_t word_begin;            // first flat u32 word index of this level
+  int nw32p;                     // nw32 rounded up to 4 (thread slots per row)
+  int64_t word_begin;            // first flat thread slot of this level
 };
 
 struct ThreshArgs {
@@ -28,10 +29,11 @@ struct ThreshArgs {
   int tol;
   int n;
   ThreshLevel lv[kMaxLevels];
-  int64_t words_per_img;         // sum over levels of h * nw32
+  int64_t words_per_img;         // sum over levels of h * nw32p
   uint32_t* mtb;                 // bitmap arena (u32 view), image stride bit_img_words*2
   uint32_t* excl;
   int64_t bit_img_words32;
+  int discard;                   // drop the consumed gray lines from L2 (no write-back)
 };
 
 // Bits of one 32-pixel word from 32 gray bytes (pixels beyond `valid` are 0).
@@ -50,6 +52,48 @@ __device__ __forceinline__ void pack32(const uint32_t (&g)[8], int valid, int me
   eb = e & keep;
 }
 
+// SWAR "x > c" for the four bytes of x at once (c a per-level constant):
+// x > c  <=>  x + (255 - c) carries out of the byte.  With xl = x & 0x7f7f7f7f
+// and yl = (255 - c) & 0x7f7f7f7f replicated, s = xl + yl never carries across
+// bytes, and the byte carry-out is MAJ(x7, y7, s7) — one LOP3.  Result: bit 7
+// of each byte (other bits are junk).
+struct GtConst {
+  uint32_t y;    // (255 - c) replicated in all four bytes
+  uint32_t yl;   // y & 0x7f7f7f7f
+};
+__device__ __forceinline__ GtConst gt_const(int c) {
+  c = c < 0 ? 0 : (c > 255 ? 255 : c);
+  const uint32_t y = (uint32_t)(255 - c) * 0x01010101u;
+  return {y, y & 0x7f7f7f7fu};
+}
+__device__ __forceinline__ uint32_t gt_bytes(uint32_t x, uint32_t xl, GtConst k) {
+  const uint32_t s = xl + k.yl;
+  return (x & k.y) | (x & s) | (k.y & s);  // majority -> one LOP3
+}
+// Bits 7,15,23,31 of m (others zero) -> bits 0..3 of the result, in order.
+__device__ __forceinline__ uint32_t gather_msb(uint32_t m) { return (m * 0x00204081u) >> 28; }
+
+// pack32 in SWAR form (about 4 instructions per pixel).  Bit-identical to
+// pack32 for 0 <= median <= 255 and tol >= 0.
+__device__ __forceinline__ void pack32_swar(const uint32_t (&g)[8], int valid, GtConst kmed, GtConst khi,
+                                            GtConst klo, uint32_t lomask, uint32_t& mtb, uint32_t& eb) {
+  constexpr uint32_t H = 0x80808080u;
+  uint32_t m = 0, e = 0;
+#pragma unroll
+  for (int k = 0; k < 8; ++k) {
+    const uint32_t x = g[k], xl = x & 0x7f7f7f7fu;
+    const uint32_t gm = gt_bytes(x, xl, kmed) & H;
+    const uint32_t gh = gt_bytes(x, xl, khi) & H;
+    const uint32_t gl = gt_bytes(x, xl, klo);                 // x > lo - 1, i.e. x >= lo
+    const uint32_t ge = gh | (~gl & lomask);                  // x > hi  or  x < lo
+    m |= gather_msb(gm) << (4 * k);
+    e |= gather_msb(ge) << (4 * k);
+  }
+  const uint32_t keep = valid >= 32 ? 0xffffffffu : (valid <= 0 ? 0u : ((1u << valid) - 1u));
+  mtb = m & keep;
+  eb = e & keep;
+}
+
 __global__ void __launch_bounds__(256) threshold_levels_kernel(ThreshArgs a) {
   const int img = blockIdx.y;
   const uint8_t* gray = a.gray + img * a.gray_img_stride;
@@ -61,16 +105,27 @@ __global__ void __launch_bounds__(256) threshold_levels_kernel(ThreshArgs a) {
     while (k + 1 < a.n && i >= a.lv[k + 1].word_begin) ++k;
     const ThreshLevel& L = a.lv[k];
     const int64_t local = i - L.word_begin;
-    const int y = (int)(local / L.nw32);
-    const int j = (int)(local - (int64_t)y * L.nw32);
+    const int y = (int)(local / L.nw32p);
+    const int j = (int)(local - (int64_t)y * L.nw32p);
+    if (j >= L.nw32) continue;  // slot padding (rows hold a multiple of 4 slots)
     const int x0 = 32 * j;
     uint32_t mw = 0, ew = 0;
     if (x0 < L.w) {
-      // gray pitch is a multiple of 64 bytes, so these 32 bytes are in-bounds and aligned.
-      const uint4* p = reinterpret_cast<const uint4*>(gray + L.gray_off + (int64_t)y * L.gray_pitch + x0);
-      const uint4 v0 = __ldg(p), v1 = __ldg(p + 1);
+      // gray pitch is a multiple of 128 bytes, so these 32 bytes are in-bounds and aligned.
+      const uint8_t* src = gray + L.gray_off + (int64_t)y * L.gray_pitch + x0;
+      const uint4* p = reinterpret_cast<const uint4*>(src);
+      const uint4 v0 = __ldcs(p), v1 = __ldcs(p + 1);
       const uint32_t g[8] = {v0.x, v0.y, v0.z, v0.w, v1.x, v1.y, v1.z, v1.w};
-      pack32(g, L.w - x0, a.medians[img * a.n + k], a.tol, mw, ew);
+      const int med = a.medians[img * a.n + k];
+      const int lo = med - a.tol;
+      pack32_swar(g, L.w - x0, gt_const(med), gt_const(med + a.tol), gt_const(lo - 1),
+                  lo > 0 ? 0x80808080u : 0u, mw, ew);
+      if (a.discard) {
+        // The 4 slots of one 128-B line are 4 consecutive lanes of this warp
+        // (rows start at multiples of 4 slots); drop the line once all read it.
+        __syncwarp(__activemask());
+        if ((j & 3) == 0) asm volatile("discard.global.L2 [%0], 128;" ::"l"(src) : "memory");
+      }
     }
     const int64_t o = 2 * L.bit_off + (int64_t)y * L.nw32 + j;
     mtb[o] = mw;
@@ -149,7 +204,7 @@ __global__ void lut_kernel(const uint8_t* __restrict__ in, const uint8_t* __rest
 }
 
 int launch_threshold_levels(const uint8_t* gray, const Plan& p, int n_img, const int32_t* medians, int tol,
-                            uint64_t* mtb, uint64_t* excl, cudaStream_t st) {
+                            uint64_t* mtb, uint64_t* excl, int discard, cudaStream_t st) {
   ThreshArgs a{};
   a.gray = gray;
   a.gray_img_stride = p.gray_img_bytes;
@@ -165,13 +220,15 @@ int launch_threshold_levels(const uint8_t* gray, const Plan& p, int n_img, const
     L.gray_pitch = p.lv[k].gray_pitch;
     L.bit_off = p.lv[k].bit_off;
     L.nw32 = (int)(2 * p.lv[k].nw64);
+    L.nw32p = (L.nw32 + 3) & ~3;
     L.word_begin = words;
-    words += (int64_t)L.h * L.nw32;
+    words += (int64_t)L.h * L.nw32p;
   }
   a.words_per_img = words;
   a.mtb = reinterpret_cast<uint32_t*>(mtb);
   a.excl = reinterpret_cast<uint32_t*>(excl);
   a.bit_img_words32 = 2 * p.bit_img_words;
+  a.discard = discard;
   int64_t per_img = (int64_t)num_sms() * 8 / (n_img > 0 ? n_img : 1);
   if (per_img < 1) per_img = 1;
   const int64_t need = (words + 255) / 256;

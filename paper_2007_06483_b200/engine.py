@@ -102,12 +102,15 @@ class MtbEngine:
         _lib.call("mtb_pyramid_hist", p["rgb"], 3 * self.width, 3 * self.width * self.height,
                   self.width, self.height, count, self.requested_levels, p["gray"], p["hist_ws"], _dev.stream())
 
-    def threshold_levels(self, pyr: PyramidSet, n_img: int, i0: int = 0):
-        """Stage 2: medians + MTB/exclusion packing of every level of images [i0, i0+n_img)."""
+    def threshold_levels(self, pyr: PyramidSet, n_img: int, i0: int = 0, discard_gray: bool = False):
+        """Stage 2: medians + MTB/exclusion packing of every level of images [i0, i0+n_img).
+
+        discard_gray drops the consumed gray lines from L2 without write-back
+        (the gray arena is undefined afterwards)."""
         p = self._ptrs(None, pyr, i0)
         _lib.call("mtb_threshold_levels", p["gray"], p["hist_ws"], self.width, self.height,
                   n_img, self.requested_levels, self.tol, p["hist"], p["medians"], p["mtb"], p["excl"],
-                  _dev.stream())
+                  1 if discard_gray else 0, _dev.stream())
 
     def preprocess_range(self, rgb, pyr: PyramidSet, i0: int, count: int):
         """Fused preprocess (all three kernels) of images [i0, i0+count) into their arena slots."""

@@ -44,7 +44,7 @@ def test_plan_matches_reference_pyramid(w, h, L):
     for k in range(n):
         lw, lh, pitch, goff, nw64, boff = (int(v) for v in geom[k])
         assert (lw, lh) == (gw, gh)                  # floor halving, pyramid.py:29
-        assert pitch % 64 == 0 and pitch >= lw
+        assert pitch % 128 == 0 and pitch >= lw
         assert nw64 == (lw + 63) // 64                # bitmap.py:35
         assert goff % 256 == 0 and goff >= prev_gray_end
         assert boff % 32 == 0 and boff >= prev_bit_end
