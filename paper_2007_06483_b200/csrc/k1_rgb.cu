@@ -28,6 +28,8 @@
 #include <cuda.h>
 #include <cudaTypedefs.h>
 
+#include <type_traits>
+
 #include "common.cuh"
 
 namespace cg = cooperative_groups;
@@ -50,7 +52,7 @@ struct K1Args {
   int nl;                 // levels produced (1..6)
   uint32_t* hist;         // spread histograms [img][level][bin * 32]
   int64_t hist_img_stride;
-  int tiles_x, tiles_y;   // interior (full) tiles only: w/128 x h/32
+  int tiles_x, tiles_y;   // ceil(w/128) x ceil(h/32)
   int cluster;            // CTAs per cluster (1, 2, 4)
 };
 
@@ -65,7 +67,6 @@ struct alignas(128) GroupSmem {
 
 struct K1Smem {
   GroupSmem grp[kK1Groups];
-  uint32_t hist[6 * 256];
 };
 
 __device__ __forceinline__ uint32_t smem_addr(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
@@ -147,7 +148,7 @@ __device__ __forceinline__ uint32_t pack_box(uint32_t q0, uint32_t q1) { return 
 __global__ void __launch_bounds__(kK1Threads, 1) k1_rgb_pyramid_kernel(K1Args a, const __grid_constant__ CUtensorMap rgb_map) {
   extern __shared__ __align__(128) uint8_t k1_smem_raw[];
   K1Smem& SM = *reinterpret_cast<K1Smem*>(k1_smem_raw);
-  uint32_t* s_hist = SM.hist;
+  __shared__ uint32_t s_hist[6 * 256];   // static: its base folds into the ATOMS immediate
 
   const int tid = threadIdx.x;
   const int g = tid >> 7;             // group
@@ -187,78 +188,116 @@ __global__ void __launch_bounds__(kK1Threads, 1) k1_rgb_pyramid_kernel(K1Args a,
   if (t_begin + g + kK1Groups < t_end) issue(t_begin + g + kK1Groups, 1);
 
   int iter = 0;
+  int ty = (t_begin + g) / a.tiles_x, tx = (t_begin + g) - ty * a.tiles_x;
   for (int tile = t_begin + g; tile < t_end; tile += kK1Groups, ++iter) {
-    const int ty = tile / a.tiles_x, tx = tile - ty * a.tiles_x;
+    if (iter) {  // advance (ty, tx) by kK1Groups tiles without a division
+      tx += kK1Groups;
+      while (tx >= a.tiles_x) { tx -= a.tiles_x; ++ty; }
+    }
     const int y0 = ty * 32 + 2 * ry, x0 = tx * 128 + 16 * cx;
     const int stage = iter & 1;
+    // Interior tiles need no bounds checks; edge tiles (TMA zero-fills what
+    // lies outside the image) mask their histogram counts and row stores.
+    const bool full = (ty * 32 + 32 <= a.h) && (tx * 128 + 128 <= a.w);
 
-    // ---- level 0: 2 rows x 16 pixels --------------------------------------
-    uint32_t gw[2][4];
-    {
-      mbar_wait(&S.full[stage], (iter >> 1) & 1);
-      const uint8_t* p0 = S.rgb[stage] + (2 * ry) * 384 + 48 * cx;
-      const uint8_t* p1 = p0 + 384;
-      const uint4 q0 = *reinterpret_cast<const uint4*>(p0), q1 = *reinterpret_cast<const uint4*>(p0 + 16),
-                  q2 = *reinterpret_cast<const uint4*>(p0 + 32);
-      const uint4 q3 = *reinterpret_cast<const uint4*>(p1), q4 = *reinterpret_cast<const uint4*>(p1 + 16),
-                  q5 = *reinterpret_cast<const uint4*>(p1 + 32);
-      const uint32_t wv[2][12] = {{q0.x, q0.y, q0.z, q0.w, q1.x, q1.y, q1.z, q1.w, q2.x, q2.y, q2.z, q2.w},
-                                  {q3.x, q3.y, q3.z, q3.w, q4.x, q4.y, q4.z, q4.w, q5.x, q5.y, q5.z, q5.w}};
+    auto body = [&](auto full_tag) {
+      constexpr bool FULL = decltype(full_tag)::value;
+      // ---- level 0: 2 rows x 16 pixels ------------------------------------
+      uint32_t gw[2][4];
+      {
+        mbar_wait(&S.full[stage], (iter >> 1) & 1);
+        const uint8_t* p0 = S.rgb[stage] + (2 * ry) * 384 + 48 * cx;
+        const uint8_t* p1 = p0 + 384;
+        const uint4 q0 = *reinterpret_cast<const uint4*>(p0), q1 = *reinterpret_cast<const uint4*>(p0 + 16),
+                    q2 = *reinterpret_cast<const uint4*>(p0 + 32);
+        const uint4 q3 = *reinterpret_cast<const uint4*>(p1), q4 = *reinterpret_cast<const uint4*>(p1 + 16),
+                    q5 = *reinterpret_cast<const uint4*>(p1 + 32);
+        const uint32_t wv[2][12] = {{q0.x, q0.y, q0.z, q0.w, q1.x, q1.y, q1.z, q1.w, q2.x, q2.y, q2.z, q2.w},
+                                    {q3.x, q3.y, q3.z, q3.w, q4.x, q4.y, q4.z, q4.w, q5.x, q5.y, q5.z, q5.w}};
+        const int nvx = FULL ? 16 : min(16, max(0, a.w - x0));
 #pragma unroll
-      for (int j = 0; j < 2; ++j) {
+        for (int j = 0; j < 2; ++j) {
+          const bool row_ok = FULL || (y0 + j < a.h);
 #pragma unroll
-        for (int k = 0; k < 4; ++k) {
-          uint32_t s4[4];
-          gw[j][k] = gray4(wv[j][3 * k], wv[j][3 * k + 1], wv[j][3 * k + 2], s4);
+          for (int k = 0; k < 4; ++k) {
+            uint32_t s4[4];
+            gw[j][k] = gray4(wv[j][3 * k], wv[j][3 * k + 1], wv[j][3 * k + 2], s4);
 #pragma unroll
-          for (int i = 0; i < 4; ++i) atomicAdd(&s_hist[s4[i] >> 8], 1u);
+            for (int i = 0; i < 4; ++i) {
+              if (FULL) {
+                atomicAdd(&s_hist[s4[i] >> 8], 1u);
+              } else if (row_ok && 4 * k + i < nvx) {
+                atomicAdd(&s_hist[s4[i] >> 8], 1u);
+              }
+            }
+          }
+          if (row_ok)
+            *reinterpret_cast<uint4*>(gray + a.off[0] + (int64_t)(y0 + j) * a.pitch[0] + x0) =
+                make_uint4(gw[j][0], gw[j][1], gw[j][2], gw[j][3]);
         }
-        *reinterpret_cast<uint4*>(gray + a.off[0] + (int64_t)(y0 + j) * a.pitch[0] + x0) =
-            make_uint4(gw[j][0], gw[j][1], gw[j][2], gw[j][3]);
       }
-    }
-    if (a.nl >= 2) {
-    // ---- level 1: 1 row x 8 pixels, in registers --------------------------
-    uint32_t l1[2];
-    {
-      l1[0] = pack_box(box2(gw[0][0], gw[1][0]), box2(gw[0][1], gw[1][1]));
-      l1[1] = pack_box(box2(gw[0][2], gw[1][2]), box2(gw[0][3], gw[1][3]));
-      *reinterpret_cast<uint2*>(gray + a.off[1] + (int64_t)(ty * 16 + ry) * a.pitch[1] + tx * 64 + 8 * cx) =
-          make_uint2(l1[0], l1[1]);
+      if (a.nl < 2) return;
+
+      // ---- level 1: 1 row x 8 pixels, in registers ------------------------
+      uint32_t l1[2];
+      {
+        l1[0] = pack_box(box2(gw[0][0], gw[1][0]), box2(gw[0][1], gw[1][1]));
+        l1[1] = pack_box(box2(gw[0][2], gw[1][2]), box2(gw[0][3], gw[1][3]));
+        const int y = ty * 16 + ry, x = tx * 64 + 8 * cx;
+        if (FULL || y < a.lh[1]) {
+          *reinterpret_cast<uint2*>(gray + a.off[1] + (int64_t)y * a.pitch[1] + x) = make_uint2(l1[0], l1[1]);
+          const int nv = FULL ? 8 : min(8, max(0, a.lw[1] - x));
 #pragma unroll
-      for (int i = 0; i < 8; ++i) atomicAdd(&s_hist[256 + ((l1[i >> 2] >> (8 * (i & 3))) & 0xff)], 1u);
-    }
-    if (a.nl >= 3) {
-    // ---- level 2: partner ry^1 (lane^8); even-ry thread emits 4 pixels ----
-    uint32_t l2 = 0;
-    {
-      const uint32_t o0 = __shfl_xor_sync(0xffffffffu, l1[0], 8);
-      const uint32_t o1 = __shfl_xor_sync(0xffffffffu, l1[1], 8);
-      if ((ry & 1) == 0) {
-        l2 = pack_box(box2(l1[0], o0), box2(l1[1], o1));
-        *reinterpret_cast<uint32_t*>(gray + a.off[2] + (int64_t)(ty * 8 + (ry >> 1)) * a.pitch[2] + tx * 32 +
-                                     4 * cx) = l2;
+          for (int i = 0; i < 8; ++i) {
+            if (FULL || i < nv) atomicAdd(&s_hist[256 + ((l1[i >> 2] >> (8 * (i & 3))) & 0xff)], 1u);
+          }
+        }
+      }
+      if (a.nl < 3) return;
+
+      // ---- level 2: partner ry^1 (lane^8); even-ry thread emits 4 pixels --
+      uint32_t l2 = 0;
+      {
+        const uint32_t o0 = __shfl_xor_sync(0xffffffffu, l1[0], 8);
+        const uint32_t o1 = __shfl_xor_sync(0xffffffffu, l1[1], 8);
+        if ((ry & 1) == 0) {
+          l2 = pack_box(box2(l1[0], o0), box2(l1[1], o1));
+          const int y = ty * 8 + (ry >> 1), x = tx * 32 + 4 * cx;
+          if (FULL || y < a.lh[2]) {
+            *reinterpret_cast<uint32_t*>(gray + a.off[2] + (int64_t)y * a.pitch[2] + x) = l2;
+            const int nv = FULL ? 4 : min(4, max(0, a.lw[2] - x));
 #pragma unroll
-        for (int i = 0; i < 4; ++i) atomicAdd(&s_hist[512 + ((l2 >> (8 * i)) & 0xff)], 1u);
+            for (int i = 0; i < 4; ++i) {
+              if (FULL || i < nv) atomicAdd(&s_hist[512 + ((l2 >> (8 * i)) & 0xff)], 1u);
+            }
+          }
+        }
       }
-    }
-    if (a.nl >= 4) {
-    // ---- level 3: partner ry^2 (lane^16); ry%4==0 thread emits 2 pixels ---
-    {
-      const uint32_t o = __shfl_xor_sync(0xffffffffu, l2, 16);
-      if ((ry & 3) == 0) {
-        const uint32_t q = box2(l2, o);
-        const uint32_t v0 = q & 0xff, v1 = (q >> 16) & 0xff;
-        const uint16_t pk = (uint16_t)(v0 | (v1 << 8));
-        const int r3 = ry >> 2;  // 0..3
-        *reinterpret_cast<uint16_t*>(&S.l3[iter & 1][r3 * 16 + 2 * cx]) = pk;
-        *reinterpret_cast<uint16_t*>(gray + a.off[3] + (int64_t)(ty * 4 + r3) * a.pitch[3] + tx * 16 + 2 * cx) =
-            pk;
-        atomicAdd(&s_hist[768 + v0], 1u);
-        atomicAdd(&s_hist[768 + v1], 1u);
+      if (a.nl < 4) return;
+
+      // ---- level 3: partner ry^2 (lane^16); ry%4==0 thread emits 2 pixels -
+      {
+        const uint32_t o = __shfl_xor_sync(0xffffffffu, l2, 16);
+        if ((ry & 3) == 0) {
+          const uint32_t q = box2(l2, o);
+          const uint32_t v0 = q & 0xff, v1 = (q >> 16) & 0xff;
+          const uint16_t pk = (uint16_t)(v0 | (v1 << 8));
+          const int r3 = ry >> 2;  // 0..3
+          *reinterpret_cast<uint16_t*>(&S.l3[iter & 1][r3 * 16 + 2 * cx]) = pk;
+          const int y = ty * 4 + r3, x = tx * 16 + 2 * cx;
+          if (FULL || y < a.lh[3]) {
+            *reinterpret_cast<uint16_t*>(gray + a.off[3] + (int64_t)y * a.pitch[3] + x) = pk;
+            if (FULL || x < a.lw[3]) atomicAdd(&s_hist[768 + v0], 1u);
+            if (FULL || x + 1 < a.lw[3]) atomicAdd(&s_hist[768 + v1], 1u);
+          }
+        }
       }
-    }
-    }}}
+    };
+    if (full)
+      body(std::true_type{});
+    else
+      body(std::false_type{});
+
     group_bar(g);  // every thread has consumed ring stage `stage` (and written l3)
     if (tile + 2 * kK1Groups < t_end) {
       if (t == 0) asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
@@ -274,15 +313,21 @@ __global__ void __launch_bounds__(kK1Threads, 1) k1_rgb_pyramid_kernel(K1Args a,
         const uint8_t* sp = l3 + (2 * r) * 16 + 2 * c;
         const uint32_t v = (sp[0] + sp[1] + sp[16] + sp[17] + 2u) >> 2;
         S.l4[r * 8 + c] = (uint8_t)v;
-        gray[a.off[4] + (int64_t)(ty * 2 + r) * a.pitch[4] + tx * 8 + c] = (uint8_t)v;
-        atomicAdd(&s_hist[1024 + v], 1u);
+        const int y = ty * 2 + r, x = tx * 8 + c;
+        if (full || (y < a.lh[4] && x < a.lw[4])) {
+          gray[a.off[4] + (int64_t)y * a.pitch[4] + x] = (uint8_t)v;
+          atomicAdd(&s_hist[1024 + v], 1u);
+        }
       }
       __syncwarp();
       if (a.nl > 5 && lane < 4) {  // level 5: 1 x 4
         const uint8_t* sp = S.l4 + 2 * lane;
         const uint32_t v = (sp[0] + sp[1] + sp[8] + sp[9] + 2u) >> 2;
-        gray[a.off[5] + (int64_t)ty * a.pitch[5] + tx * 4 + lane] = (uint8_t)v;
-        atomicAdd(&s_hist[1280 + v], 1u);
+        const int y = ty, x = tx * 4 + lane;
+        if (full || (y < a.lh[5] && x < a.lw[5])) {
+          gray[a.off[5] + (int64_t)y * a.pitch[5] + x] = (uint8_t)v;
+          atomicAdd(&s_hist[1280 + v], 1u);
+        }
       }
       __syncwarp();
     }
@@ -347,8 +392,8 @@ int launch_k1_rgb(const uint8_t* rgb, int64_t rgb_pitch, int64_t rgb_img_stride,
     a.lh[k] = k < p.n ? p.lv[k].h : 0;
   }
   a.hist_img_stride = hist_img_stride;
-  a.tiles_x = a.w / 128;   // interior tiles; edge tiles go to the generic kernel
-  a.tiles_y = a.h / 32;
+  a.tiles_x = (a.w + 127) / 128;   // edge tiles included: TMA zero-fills outside the image
+  a.tiles_y = (a.h + 31) / 32;
   const int ntiles = a.tiles_x * a.tiles_y;
   if (ntiles == 0) return MTB_OK;
   static bool attr_done = false;

@@ -390,10 +390,10 @@ int launch_pyramid(const uint8_t* rgb, int64_t rgb_pitch, int64_t rgb_img_stride
     a.hist_level0 = 0;
     a.tiles_x = (int)((a.src_w + kTileCols - 1) / kTileCols);
     a.tiles_y = (int)((a.src_h + kTileRows - 1) / kTileRows);
-    a.edge_only = vec_ok ? 1 : 0;
-    const int64_t n_edge = ((a.src_w % kTileCols) ? a.tiles_y : 0) +
-                           ((a.src_h % kTileRows) ? a.tiles_x - ((a.src_w % kTileCols) ? 1 : 0) : 0);
-    const int64_t ntiles = vec_ok ? n_edge : (int64_t)a.tiles_x * a.tiles_y;
+    a.edge_only = 0;
+    // The TMA kernel covers every tile (edges included); the generic kernel
+    // only runs when the RGB rows do not allow the tensor map.
+    const int64_t ntiles = vec_ok ? 0 : (int64_t)a.tiles_x * a.tiles_y;
     if (ntiles > 0) {
       int64_t per_img = (int64_t)num_sms() * 4 / (n_img > 0 ? n_img : 1);
       if (per_img < 1) per_img = 1;

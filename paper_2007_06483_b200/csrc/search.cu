@@ -160,19 +160,42 @@ level_search_kernel(LevelSearchArgs a) {
   const int64_t sj0 = (int64_t)j0 - qb - 2;  // first staged source word
 
   // ---- stage (all loads in flight together) ----
-  for (int i = tid; i < kSTRows * kSTWords; i += kSTThreads) {
+  constexpr int kAPer = kSTRows * kSTWords / kSTThreads;                      // 8
+  constexpr int kBPer = (kSTBRows * kSTBWords + kSTThreads - 1) / kSTThreads;  // 10
+  uint32_t ra[kAPer], rea[kAPer], rb[kBPer], reb[kBPer];
+#pragma unroll
+  for (int u = 0; u < kAPer; ++u) {
+    const int i = tid + u * kSTThreads;
     const int r = i / kSTWords, c = i - r * kSTWords;
     const int y = y0 + r, j = j0 + c;
     const bool ok = y < a.h && j < a.nw32;
-    S.a[r][c] = ok ? __ldg(A + (int64_t)y * a.nw32 + j) : 0u;
-    S.ea[r][c] = ok ? __ldg(EA + (int64_t)y * a.nw32 + j) : 0u;
+    ra[u] = ok ? __ldg(A + (int64_t)y * a.nw32 + j) : 0u;
+    rea[u] = ok ? __ldg(EA + (int64_t)y * a.nw32 + j) : 0u;
   }
-  for (int i = tid; i < kSTBRows * kSTBWords; i += kSTThreads) {
+#pragma unroll
+  for (int u = 0; u < kBPer; ++u) {
+    const int i = tid + u * kSTThreads;
     const int r = i / kSTBWords, c = i - r * kSTBWords;
     const int64_t y = (int64_t)sy0 + r, j = sj0 + c;
-    const bool ok = y >= 0 && y < a.h && j >= 0 && j < a.nw32;
-    S.b[r][c] = ok ? __ldg(B + y * a.nw32 + j) : 0u;
-    S.eb[r][c] = ok ? __ldg(EB + y * a.nw32 + j) : 0u;
+    const bool ok = i < kSTBRows * kSTBWords && y >= 0 && y < a.h && j >= 0 && j < a.nw32;
+    rb[u] = ok ? __ldg(B + y * a.nw32 + j) : 0u;
+    reb[u] = ok ? __ldg(EB + y * a.nw32 + j) : 0u;
+  }
+#pragma unroll
+  for (int u = 0; u < kAPer; ++u) {
+    const int i = tid + u * kSTThreads;
+    const int r = i / kSTWords, c = i - r * kSTWords;
+    S.a[r][c] = ra[u];
+    S.ea[r][c] = rea[u];
+  }
+#pragma unroll
+  for (int u = 0; u < kBPer; ++u) {
+    const int i = tid + u * kSTThreads;
+    if (i < kSTBRows * kSTBWords) {
+      const int r = i / kSTBWords, c = i - r * kSTBWords;
+      S.b[r][c] = rb[u];
+      S.eb[r][c] = reb[u];
+    }
   }
   __syncthreads();
 

@@ -18,8 +18,7 @@ struct ThreshLevel {
   int64_t gray_off, gray_pitch;  // bytes (pitch is a multiple of 128)
   int64_t bit_off;               // u64 words
   int nw32;                      // u32 words per packed row
-  int nw32p;                     // nw32 rounded up to 4 (thread slots per row)
-  int64_t word_begin;            // first flat thread slot of this level
+  int row_begin;                 // first flat row of this level (levels concatenated)
 };
 
 struct ThreshArgs {
@@ -29,7 +28,7 @@ struct ThreshArgs {
   int tol;
   int n;
   ThreshLevel lv[kMaxLevels];
-  int64_t words_per_img;         // sum over levels of h * nw32p
+  int rows_per_img;              // sum over levels of h
   uint32_t* mtb;                 // bitmap arena (u32 view), image stride bit_img_words*2
   uint32_t* excl;
   int64_t bit_img_words32;
@@ -94,42 +93,46 @@ __device__ __forceinline__ void pack32_swar(const uint32_t (&g)[8], int valid, G
   eb = e & keep;
 }
 
+// One warp per packed row (rows of all levels concatenated); lane j handles
+// words j, j+32, ... of the row, i.e. 32 pixels = 32 aligned gray bytes each.
 __global__ void __launch_bounds__(256) threshold_levels_kernel(ThreshArgs a) {
   const int img = blockIdx.y;
+  const int lane = threadIdx.x & 31;
   const uint8_t* gray = a.gray + img * a.gray_img_stride;
   uint32_t* mtb = a.mtb + img * a.bit_img_words32;
   uint32_t* excl = a.excl + img * a.bit_img_words32;
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < a.words_per_img;
-       i += (int64_t)gridDim.x * blockDim.x) {
+  const int wpc = blockDim.x >> 5;
+  for (int row = blockIdx.x * wpc + (threadIdx.x >> 5); row < a.rows_per_img; row += gridDim.x * wpc) {
     int k = 0;
-    while (k + 1 < a.n && i >= a.lv[k + 1].word_begin) ++k;
+    while (k + 1 < a.n && row >= a.lv[k + 1].row_begin) ++k;
     const ThreshLevel& L = a.lv[k];
-    const int64_t local = i - L.word_begin;
-    const int y = (int)(local / L.nw32p);
-    const int j = (int)(local - (int64_t)y * L.nw32p);
-    if (j >= L.nw32) continue;  // slot padding (rows hold a multiple of 4 slots)
-    const int x0 = 32 * j;
-    uint32_t mw = 0, ew = 0;
-    if (x0 < L.w) {
-      // gray pitch is a multiple of 128 bytes, so these 32 bytes are in-bounds and aligned.
-      const uint8_t* src = gray + L.gray_off + (int64_t)y * L.gray_pitch + x0;
-      const uint4* p = reinterpret_cast<const uint4*>(src);
-      const uint4 v0 = __ldcs(p), v1 = __ldcs(p + 1);
-      const uint32_t g[8] = {v0.x, v0.y, v0.z, v0.w, v1.x, v1.y, v1.z, v1.w};
-      const int med = a.medians[img * a.n + k];
-      const int lo = med - a.tol;
-      pack32_swar(g, L.w - x0, gt_const(med), gt_const(med + a.tol), gt_const(lo - 1),
-                  lo > 0 ? 0x80808080u : 0u, mw, ew);
-      if (a.discard) {
-        // The 4 slots of one 128-B line are 4 consecutive lanes of this warp
-        // (rows start at multiples of 4 slots); drop the line once all read it.
-        __syncwarp(__activemask());
-        if ((j & 3) == 0) asm volatile("discard.global.L2 [%0], 128;" ::"l"(src) : "memory");
+    const int y = row - L.row_begin;
+    const int med = a.medians[img * a.n + k];
+    const int lo = med - a.tol;
+    const GtConst kmed = gt_const(med), khi = gt_const(med + a.tol), klo = gt_const(lo - 1);
+    const uint32_t lomask = lo > 0 ? 0x80808080u : 0u;
+    const uint8_t* grow = gray + L.gray_off + (int64_t)y * L.gray_pitch;
+    uint32_t* mrow = mtb + 2 * L.bit_off + (int64_t)y * L.nw32;
+    uint32_t* erow = excl + 2 * L.bit_off + (int64_t)y * L.nw32;
+    for (int j = lane; j < L.nw32; j += 32) {
+      const int x0 = 32 * j;
+      uint32_t mw = 0, ew = 0;
+      if (x0 < L.w) {
+        // gray pitch is a multiple of 128 bytes: these 32 bytes are in-bounds and aligned.
+        const uint4* p = reinterpret_cast<const uint4*>(grow + x0);
+        const uint4 v0 = __ldcs(p), v1 = __ldcs(p + 1);
+        const uint32_t g[8] = {v0.x, v0.y, v0.z, v0.w, v1.x, v1.y, v1.z, v1.w};
+        pack32_swar(g, L.w - x0, kmed, khi, klo, lomask, mw, ew);
+        if (a.discard) {
+          // words j..j+3 share one 128-B line and are lanes of this iteration;
+          // drop the line from L2 (no write-back) once all of them read it.
+          __syncwarp(__activemask());
+          if ((j & 3) == 0) asm volatile("discard.global.L2 [%0], 128;" ::"l"(grow + x0) : "memory");
+        }
       }
+      mrow[j] = mw;
+      erow[j] = ew;
     }
-    const int64_t o = 2 * L.bit_off + (int64_t)y * L.nw32 + j;
-    mtb[o] = mw;
-    excl[o] = ew;
   }
 }
 
@@ -211,7 +214,7 @@ int launch_threshold_levels(const uint8_t* gray, const Plan& p, int n_img, const
   a.medians = medians;
   a.tol = tol;
   a.n = p.n;
-  int64_t words = 0;
+  int rows = 0;
   for (int k = 0; k < p.n; ++k) {
     ThreshLevel& L = a.lv[k];
     L.w = p.lv[k].w;
@@ -220,18 +223,17 @@ int launch_threshold_levels(const uint8_t* gray, const Plan& p, int n_img, const
     L.gray_pitch = p.lv[k].gray_pitch;
     L.bit_off = p.lv[k].bit_off;
     L.nw32 = (int)(2 * p.lv[k].nw64);
-    L.nw32p = (L.nw32 + 3) & ~3;
-    L.word_begin = words;
-    words += (int64_t)L.h * L.nw32p;
+    L.row_begin = rows;
+    rows += L.h;
   }
-  a.words_per_img = words;
+  a.rows_per_img = rows;
   a.mtb = reinterpret_cast<uint32_t*>(mtb);
   a.excl = reinterpret_cast<uint32_t*>(excl);
   a.bit_img_words32 = 2 * p.bit_img_words;
   a.discard = discard;
   int64_t per_img = (int64_t)num_sms() * 8 / (n_img > 0 ? n_img : 1);
   if (per_img < 1) per_img = 1;
-  const int64_t need = (words + 255) / 256;
+  const int64_t need = (rows + 7) / 8;   // 8 warps (rows) per CTA
   if (per_img > need) per_img = need;
   threshold_levels_kernel<<<dim3((unsigned)per_img, (unsigned)n_img), 256, 0, st>>>(a);
   return check_launch("threshold_levels_kernel");
