@@ -28,6 +28,7 @@
 #include <cuda.h>
 #include <cudaTypedefs.h>
 
+#include <cstdlib>
 #include <type_traits>
 
 #include "common.cuh"
@@ -54,6 +55,7 @@ struct K1Args {
   int64_t hist_img_stride;
   int tiles_x, tiles_y;   // ceil(w/128) x ceil(h/32)
   int cluster;            // CTAs per cluster (1, 2, 4)
+  int probe;              // diagnostics only (MTB_K1_PROBE): 1 = stream tiles, skip all compute
 };
 
 constexpr int kTileRgbBytes = 32 * 384;   // one 32x128 tile of RGB8
@@ -136,6 +138,21 @@ __device__ __forceinline__ uint32_t box2(uint32_t u, uint32_t d) {
                      0x00020002u;
   return s >> 2;
 }
+// 2x2 box sum + 2 of the byte pair `pair` (0: bytes 0-1, 1: bytes 2-3) of a
+// word of the upper row u and of the lower row d: (a+b+c+d+2), < 1024.  The
+// average is sum >> 2 and its histogram byte offset is sum & 0x3fc.
+__device__ __forceinline__ uint32_t box_sum(uint32_t u, uint32_t d, int pair) {
+  const uint32_t w = pair ? 0x01010000u : 0x00000101u;
+  return __dp4a(u, w, __dp4a(d, w, 2u));
+}
+// Four box sums -> four packed average bytes.
+__device__ __forceinline__ uint32_t pack_sums(uint32_t s0, uint32_t s1, uint32_t s2, uint32_t s3) {
+  const uint32_t x01 = (s0 + (s1 << 16)) >> 2, x23 = (s2 + (s3 << 16)) >> 2;
+  return __byte_perm(x01, x23, 0x6420);
+}
+// Increment the counter at byte offset `off` of the (static) histogram array;
+// written as plain C++ on the array so the base folds into the ATOMS address.
+__device__ __forceinline__ void hist_inc(uint32_t* hist, uint32_t off) { atomicAdd(&hist[off >> 2], 1u); }
 // Pack the two results of two box2 words into 4 consecutive bytes.
 __device__ __forceinline__ uint32_t pack_box(uint32_t q0, uint32_t q1) { return __byte_perm(q0, q1, 0x6420); }
 
@@ -145,6 +162,10 @@ __device__ __forceinline__ uint32_t pack_box(uint32_t q0, uint32_t q1) { return 
 // registers, level 2 with one shuffle (partner ry^1 = lane^8), level 3 with
 // another (partner ry^2 = lane^16); levels 4-5 (which span warps) go through a
 // 64-byte shared buffer and one named barrier per tile.
+// CLUSTER: reduce histograms across a thread-block cluster through DSMEM.  A
+// separate instantiation, because cluster-capable code addresses its own
+// shared memory through the CTA's cluster window (an extra add per access).
+template <bool CLUSTER>
 __global__ void __launch_bounds__(kK1Threads, 1) k1_rgb_pyramid_kernel(K1Args a, const __grid_constant__ CUtensorMap rgb_map) {
   extern __shared__ __align__(128) uint8_t k1_smem_raw[];
   K1Smem& SM = *reinterpret_cast<K1Smem*>(k1_smem_raw);
@@ -224,10 +245,13 @@ __global__ void __launch_bounds__(kK1Threads, 1) k1_rgb_pyramid_kernel(K1Args a,
             gw[j][k] = gray4(wv[j][3 * k], wv[j][3 * k + 1], wv[j][3 * k + 2], s4);
 #pragma unroll
             for (int i = 0; i < 4; ++i) {
+              // 256 bins: byte offset 4*(s>>8).  (A 16K-sub-bin variant with a
+              // one-op address measured slower: fewer equal addresses per warp
+              // for ATOMS.POPC.INC to aggregate.)
               if (FULL) {
-                atomicAdd(&s_hist[s4[i] >> 8], 1u);
+                hist_inc(s_hist, (s4[i] >> 6) & 0x3fcu);
               } else if (row_ok && 4 * k + i < nvx) {
-                atomicAdd(&s_hist[s4[i] >> 8], 1u);
+                hist_inc(s_hist, (s4[i] >> 6) & 0x3fcu);
               }
             }
           }
@@ -241,15 +265,18 @@ __global__ void __launch_bounds__(kK1Threads, 1) k1_rgb_pyramid_kernel(K1Args a,
       // ---- level 1: 1 row x 8 pixels, in registers ------------------------
       uint32_t l1[2];
       {
-        l1[0] = pack_box(box2(gw[0][0], gw[1][0]), box2(gw[0][1], gw[1][1]));
-        l1[1] = pack_box(box2(gw[0][2], gw[1][2]), box2(gw[0][3], gw[1][3]));
+        uint32_t sm[8];
+#pragma unroll
+        for (int i = 0; i < 8; ++i) sm[i] = box_sum(gw[0][i >> 1], gw[1][i >> 1], i & 1);
+        l1[0] = pack_sums(sm[0], sm[1], sm[2], sm[3]);
+        l1[1] = pack_sums(sm[4], sm[5], sm[6], sm[7]);
         const int y = ty * 16 + ry, x = tx * 64 + 8 * cx;
         if (FULL || y < a.lh[1]) {
           *reinterpret_cast<uint2*>(gray + a.off[1] + (int64_t)y * a.pitch[1] + x) = make_uint2(l1[0], l1[1]);
           const int nv = FULL ? 8 : min(8, max(0, a.lw[1] - x));
 #pragma unroll
           for (int i = 0; i < 8; ++i) {
-            if (FULL || i < nv) atomicAdd(&s_hist[256 + ((l1[i >> 2] >> (8 * (i & 3))) & 0xff)], 1u);
+            if (FULL || i < nv) hist_inc(s_hist + 256, sm[i] & 0x3fcu);
           }
         }
       }
@@ -261,15 +288,17 @@ __global__ void __launch_bounds__(kK1Threads, 1) k1_rgb_pyramid_kernel(K1Args a,
         const uint32_t o0 = __shfl_xor_sync(0xffffffffu, l1[0], 8);
         const uint32_t o1 = __shfl_xor_sync(0xffffffffu, l1[1], 8);
         if ((ry & 1) == 0) {
-          l2 = pack_box(box2(l1[0], o0), box2(l1[1], o1));
+          const uint32_t s0 = box_sum(l1[0], o0, 0), s1 = box_sum(l1[0], o0, 1);
+          const uint32_t s2 = box_sum(l1[1], o1, 0), s3 = box_sum(l1[1], o1, 1);
+          l2 = pack_sums(s0, s1, s2, s3);
           const int y = ty * 8 + (ry >> 1), x = tx * 32 + 4 * cx;
           if (FULL || y < a.lh[2]) {
             *reinterpret_cast<uint32_t*>(gray + a.off[2] + (int64_t)y * a.pitch[2] + x) = l2;
             const int nv = FULL ? 4 : min(4, max(0, a.lw[2] - x));
-#pragma unroll
-            for (int i = 0; i < 4; ++i) {
-              if (FULL || i < nv) atomicAdd(&s_hist[512 + ((l2 >> (8 * i)) & 0xff)], 1u);
-            }
+            if (FULL || 0 < nv) hist_inc(s_hist + 512, s0 & 0x3fcu);
+            if (FULL || 1 < nv) hist_inc(s_hist + 512, s1 & 0x3fcu);
+            if (FULL || 2 < nv) hist_inc(s_hist + 512, s2 & 0x3fcu);
+            if (FULL || 3 < nv) hist_inc(s_hist + 512, s3 & 0x3fcu);
           }
         }
       }
@@ -279,24 +308,27 @@ __global__ void __launch_bounds__(kK1Threads, 1) k1_rgb_pyramid_kernel(K1Args a,
       {
         const uint32_t o = __shfl_xor_sync(0xffffffffu, l2, 16);
         if ((ry & 3) == 0) {
-          const uint32_t q = box2(l2, o);
-          const uint32_t v0 = q & 0xff, v1 = (q >> 16) & 0xff;
+          const uint32_t s0 = box_sum(l2, o, 0), s1 = box_sum(l2, o, 1);
+          const uint32_t v0 = s0 >> 2, v1 = s1 >> 2;
           const uint16_t pk = (uint16_t)(v0 | (v1 << 8));
           const int r3 = ry >> 2;  // 0..3
           *reinterpret_cast<uint16_t*>(&S.l3[iter & 1][r3 * 16 + 2 * cx]) = pk;
           const int y = ty * 4 + r3, x = tx * 16 + 2 * cx;
           if (FULL || y < a.lh[3]) {
             *reinterpret_cast<uint16_t*>(gray + a.off[3] + (int64_t)y * a.pitch[3] + x) = pk;
-            if (FULL || x < a.lw[3]) atomicAdd(&s_hist[768 + v0], 1u);
-            if (FULL || x + 1 < a.lw[3]) atomicAdd(&s_hist[768 + v1], 1u);
+            if (FULL || x < a.lw[3]) hist_inc(s_hist + 768, s0 & 0x3fcu);
+            if (FULL || x + 1 < a.lw[3]) hist_inc(s_hist + 768, s1 & 0x3fcu);
           }
         }
       }
     };
-    if (full)
+    if (a.probe) {
+      mbar_wait(&S.full[stage], (iter >> 1) & 1);
+    } else if (full) {
       body(std::true_type{});
-    else
+    } else {
       body(std::false_type{});
+    }
 
     group_bar(g);  // every thread has consumed ring stage `stage` (and written l3)
     if (tile + 2 * kK1Groups < t_end) {
@@ -335,9 +367,10 @@ __global__ void __launch_bounds__(kK1Threads, 1) k1_rgb_pyramid_kernel(K1Args a,
 
   // ---- histogram reduction: CTA -> cluster leader (DSMEM) -> global -------
   __syncthreads();
+
   uint32_t* gh = a.hist + img * a.hist_img_stride;
   const int nbins = a.nl * 256;
-  if (a.cluster > 1) {
+  if constexpr (CLUSTER) {
     cg::cluster_group cl = cg::this_cluster();
     cl.sync();
     if (cl.block_rank() != 0) {
@@ -392,6 +425,10 @@ int launch_k1_rgb(const uint8_t* rgb, int64_t rgb_pitch, int64_t rgb_img_stride,
     a.lh[k] = k < p.n ? p.lv[k].h : 0;
   }
   a.hist_img_stride = hist_img_stride;
+  {
+    const char* pr = getenv("MTB_K1_PROBE");
+    a.probe = pr ? atoi(pr) : 0;
+  }
   a.tiles_x = (a.w + 127) / 128;   // edge tiles included: TMA zero-fills outside the image
   a.tiles_y = (a.h + 31) / 32;
   const int ntiles = a.tiles_x * a.tiles_y;
@@ -399,7 +436,8 @@ int launch_k1_rgb(const uint8_t* rgb, int64_t rgb_pitch, int64_t rgb_img_stride,
   static bool attr_done = false;
   const int smem = (int)sizeof(K1Smem);
   if (!attr_done) {
-    MTB_CUDA(cudaFuncSetAttribute(k1_rgb_pyramid_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    MTB_CUDA(cudaFuncSetAttribute(k1_rgb_pyramid_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    MTB_CUDA(cudaFuncSetAttribute(k1_rgb_pyramid_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
     attr_done = true;
   }
   const int sms = num_sms();
@@ -441,8 +479,9 @@ int launch_k1_rgb(const uint8_t* rgb, int64_t rgb_pitch, int64_t rgb_img_stride,
     attr[0].val.clusterDim.y = 1;
     attr[0].val.clusterDim.z = 1;
     cfg.attrs = attr;
-    cfg.numAttrs = 1;
-    const cudaError_t e = cudaLaunchKernelEx(&cfg, k1_rgb_pyramid_kernel, a, map);
+    cfg.numAttrs = cl > 1 ? 1 : 0;
+    const cudaError_t e = cl > 1 ? cudaLaunchKernelEx(&cfg, k1_rgb_pyramid_kernel<true>, a, map)
+                                 : cudaLaunchKernelEx(&cfg, k1_rgb_pyramid_kernel<false>, a, map);
     if (e != cudaSuccess) {
       set_error(std::string("k1_rgb_pyramid_kernel: ") + cudaGetErrorString(e));
       return MTB_ECUDA;
