@@ -167,7 +167,11 @@ int mtb_select_candidate(const unsigned long long* errs, const int32_t* offsets,
  * MTB_MAX_LEVELS x 6 int64: {w, h, gray_pitch, gray_offset, nwords64,
  * bitmap_offset_words}; sizes [host] receives {gray_image_bytes,
  * bitmap_image_words, hist_workspace_u32_per_image}.  Returns n (>= 1), or -1
- * on invalid input (image smaller than 16x16, requested < 1). */
+ * on invalid input (image smaller than 16x16, requested < 1).
+ * requested < 0 plans EXACTLY -requested levels without the 16x16 clamp: a
+ * row shard of a larger image whose level count was fixed on the full image
+ * (every level must keep >= 1 row).  The fused entry points below accept the
+ * same negative `levels`. */
 int mtb_plan_levels(int w, int h, int requested, int64_t* geom, int64_t* sizes);
 
 /* to_grayscale -> build_pyramid -> build_mtb_pyramid for a batch of images
@@ -214,6 +218,35 @@ int mtb_threshold_levels(const uint8_t* gray, const uint32_t* hist_ws, int w, in
 int mtb_find_offset_batch(const uint64_t* const* maps, const int32_t* dims, int n_levels, int P,
                           const int32_t* base, int32_t* acc, unsigned long long* errs,
                           uint32_t* done, void* stream);
+
+/* ------------------------------------------------------------------------ */
+/* 4. Row-sharded search (one gigapixel pair over several GPUs)  */
+/* ------------------------------------------------------------------------ */
+
+/* One level of search_level (search.py:53-71) over a window of rows: the
+ * reference maps hold image rows [a_row0, a_row0+a_rows) of the level, the
+ * target maps rows [b_row0, b_row0+b_rows) (the shard's rows plus halo);
+ * rows outside [0, h) or outside the target window contribute 0.  Writes the
+ * 9 partial counts per pair to errs (P x errs_stride u64, zeroed here) and
+ * does NOT decide: the caller sums the counts across shards (NCCL
+ * all-reduce) and calls mtb_decide_level.  Base offsets come from prev
+ * (2 * previous level's choice) or base (deepest level) or (0,0). */
+int mtb_search_level_rows(const uint64_t* const* maps, int w, int h, int64_t nwords64,
+                          int a_row0, int a_rows, int b_row0, int b_rows, int P,
+                          const int32_t* prev, int64_t prev_stride, const int32_t* base,
+                          unsigned long long* errs, int64_t errs_stride, void* stream);
+
+/* Threshold + pack every level with GIVEN medians (n_img x n int32): the
+ * row-sharded flow all-reduces the histograms first, so every shard
+ * thresholds with the medians of the whole image (threshold.py:80-88). */
+int mtb_threshold_levels_medians(const uint8_t* gray, int w, int h, int n_img, int levels, int tol,
+                                 const int32_t* medians, uint64_t* mtb, uint64_t* exclusion,
+                                 int discard_gray, void* stream);
+
+/* The search.py:67 key over summed counts: acc[p] = chosen offset. */
+int mtb_decide_level(const unsigned long long* errs, int64_t errs_stride,
+                     const int32_t* prev, int64_t prev_stride, const int32_t* base,
+                     int32_t* acc, int64_t acc_stride, int P, void* stream);
 
 #ifdef __cplusplus
 }

@@ -53,6 +53,11 @@ SIGNATURES = {
                        _c_void_p, _c_void_p, _c_void_p, _c_void_p],
     "mtb_find_offset_batch": [_c_void_p, _c_void_p, _i32, _i32, _c_void_p, _c_void_p, _c_void_p, _c_void_p,
                               _c_void_p],
+    "mtb_search_level_rows": [_c_void_p, _i32, _i32, _i64, _i32, _i32, _i32, _i32, _i32, _c_void_p, _i64,
+                              _c_void_p, _c_void_p, _i64, _c_void_p],
+    "mtb_threshold_levels_medians": [_c_void_p, _i32, _i32, _i32, _i32, _i32, _c_void_p, _c_void_p, _c_void_p,
+                                     _i32, _c_void_p],
+    "mtb_decide_level": [_c_void_p, _i64, _c_void_p, _i64, _c_void_p, _c_void_p, _i64, _i32, _c_void_p],
 }
 
 # Non-status entry points.

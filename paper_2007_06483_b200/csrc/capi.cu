@@ -38,10 +38,18 @@ int num_sms() {
 }
 
 bool make_plan(int w, int h, int requested, Plan* p) {
-  if (requested < 1 || w < kMinLevelSize || h < kMinLevelSize) return false;
-  const int ml = max_levels(w, h);
-  const int n = requested < ml ? requested : ml;
-  if (n > kMaxLevels) return false;
+  int n;
+  if (requested < 0) {
+    // Exact level count for a row shard of a larger image (the level count
+    // was decided on the full image): every level must keep >= 1 row/column.
+    n = -requested;
+    if (n > kMaxLevels || (w >> (n - 1)) < 1 || (h >> (n - 1)) < 1) return false;
+  } else {
+    if (requested < 1 || w < kMinLevelSize || h < kMinLevelSize) return false;
+    const int ml = max_levels(w, h);
+    n = requested < ml ? requested : ml;
+    if (n > kMaxLevels) return false;
+  }
   std::memset(p, 0, sizeof(*p));
   p->n = n;
   int64_t goff = 0, boff = 0;
@@ -151,4 +159,16 @@ extern "C" int mtb_preprocess(const uint8_t* rgb, int64_t rgb_pitch, int64_t rgb
   rc = launch_hist_median(hist_ws, n_img, p.n, hist_out, medians, st);
   if (rc) return rc;
   return launch_threshold_levels(gray, p, n_img, medians, tol, mtb, exclusion, 0, st);
+}
+
+extern "C" int mtb_threshold_levels_medians(const uint8_t* gray, int w, int h, int n_img, int levels, int tol,
+                                            const int32_t* medians, uint64_t* mtb, uint64_t* exclusion,
+                                            int discard_gray, void* stream) {
+  clear_error();
+  MTB_REQUIRE(gray && medians && mtb && exclusion, "null pointer");
+  MTB_REQUIRE(n_img >= 1 && n_img <= 65535, "image count out of range");
+  MTB_REQUIRE(tol >= 0 && tol <= 255, "noise tolerance must be in 0..255");
+  Plan p;
+  MTB_REQUIRE(make_plan(w, h, levels, &p), "invalid level plan");
+  return launch_threshold_levels(gray, p, n_img, medians, tol, mtb, exclusion, discard_gray, as_stream(stream));
 }

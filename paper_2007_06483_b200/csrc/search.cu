@@ -113,7 +113,12 @@ constexpr int kSTBPitch = kSTBWords + 1;
 
 struct LevelSearchArgs {
   const uint64_t* const* maps;   // [P][4] {ref.mtb, ref.excl, tgt.mtb, tgt.excl}
-  int w, h, nw32;
+  int w, h, nw32;                // h = rows of the whole level (image coordinates)
+  // Row windows (row sharding): the reference maps hold image rows
+  // [a_row0, a_row0 + a_rows), the target maps rows [b_row0, b_row0 + b_rows)
+  // (own rows plus halo).  Unsharded: a_row0 = b_row0 = 0, a_rows = b_rows = h.
+  int a_row0, a_rows, b_row0, b_rows;
+  int decide;                    // 1: last CTA applies the search.py:67 key; 0: counts only
   const int32_t* prev;           // previous (coarser) level's chosen offset, or nullptr
   int64_t prev_stride;
   const int32_t* base;           // explicit base [P][2] when prev == nullptr (may be nullptr)
@@ -141,7 +146,8 @@ level_search_kernel(LevelSearchArgs a) {
   const int p = blockIdx.y;
   const int tid = threadIdx.x, lane = tid & 31, wi = tid >> 5;
   const int tx = blockIdx.x % a.tiles_x, ty = blockIdx.x / a.tiles_x;
-  const int y0 = ty * kSTRows, j0 = tx * kSTWords;
+  const int ly0 = ty * kSTRows, j0 = tx * kSTWords;   // local (reference-window) row of the tile
+  const int y0 = a.a_row0 + ly0;                       // image row of the tile
   const uint32_t* A = reinterpret_cast<const uint32_t*>(a.maps[4 * p + 0]);
   const uint32_t* EA = reinterpret_cast<const uint32_t*>(a.maps[4 * p + 1]);
   const uint32_t* B = reinterpret_cast<const uint32_t*>(a.maps[4 * p + 2]);
@@ -167,19 +173,20 @@ level_search_kernel(LevelSearchArgs a) {
   for (int u = 0; u < kAPer; ++u) {
     const int i = tid + u * kSTThreads;
     const int r = i / kSTWords, c = i - r * kSTWords;
-    const int y = y0 + r, j = j0 + c;
-    const bool ok = y < a.h && j < a.nw32;
-    ra[u] = ok ? __ldg(A + (int64_t)y * a.nw32 + j) : 0u;
-    rea[u] = ok ? __ldg(EA + (int64_t)y * a.nw32 + j) : 0u;
+    const int ly = ly0 + r, j = j0 + c;
+    const bool ok = ly < a.a_rows && j < a.nw32;
+    ra[u] = ok ? __ldg(A + (int64_t)ly * a.nw32 + j) : 0u;
+    rea[u] = ok ? __ldg(EA + (int64_t)ly * a.nw32 + j) : 0u;
   }
 #pragma unroll
   for (int u = 0; u < kBPer; ++u) {
     const int i = tid + u * kSTThreads;
     const int r = i / kSTBWords, c = i - r * kSTBWords;
     const int64_t y = (int64_t)sy0 + r, j = sj0 + c;
-    const bool ok = i < kSTBRows * kSTBWords && y >= 0 && y < a.h && j >= 0 && j < a.nw32;
-    rb[u] = ok ? __ldg(B + y * a.nw32 + j) : 0u;
-    reb[u] = ok ? __ldg(EB + y * a.nw32 + j) : 0u;
+    const bool ok = i < kSTBRows * kSTBWords && y >= 0 && y < a.h && y >= a.b_row0 &&
+                    y < a.b_row0 + a.b_rows && j >= 0 && j < a.nw32;
+    rb[u] = ok ? __ldg(B + (y - a.b_row0) * a.nw32 + j) : 0u;
+    reb[u] = ok ? __ldg(EB + (y - a.b_row0) * a.nw32 + j) : 0u;
   }
 #pragma unroll
   for (int u = 0; u < kAPer; ++u) {
@@ -230,7 +237,7 @@ level_search_kernel(LevelSearchArgs a) {
 #pragma unroll
   for (int i = 0; i < 9; ++i) cnt[i] = 0;
   const int rbeg = wi * (kSTRows / kSTWarps);
-  if (y0 + rbeg < a.h) {
+  if (ly0 + rbeg < a.a_rows) {
     // output local row rr needs source local rows rr (ddy=+1), rr+1 (ddy=0), rr+2 (ddy=-1)
     uint32_t b0[3], e0[3], b1[3], e1[3];
     shifted_row(rbeg, b0, e0);
@@ -267,6 +274,7 @@ level_search_kernel(LevelSearchArgs a) {
     for (int k = 0; k < kSTWarps; ++k) v += S.part[k][tid];
     if (v) atomicAdd(&errs[tid], v);
   }
+  if (!a.decide) return;
   __threadfence();
   __syncthreads();
   if (tid == 0) S.last = (atomicAdd(&a.done[p * a.done_stride], 1u) == gridDim.x - 1);
@@ -285,6 +293,34 @@ level_search_kernel(LevelSearchArgs a) {
     a.acc[p * a.acc_stride] = bx + best % 3 - 1;
     a.acc[p * a.acc_stride + 1] = by + best / 3 - 1;
   }
+}
+
+// The search.py:67 decision for P pairs from already-summed error counts
+// (row-sharded search: counts are all-reduced across ranks first).
+__global__ void decide_level_kernel(const unsigned long long* __restrict__ errs, int64_t errs_stride,
+                                    const int32_t* __restrict__ prev, int64_t prev_stride,
+                                    const int32_t* __restrict__ base, int32_t* __restrict__ acc, int64_t acc_stride,
+                                    int P) {
+  const int p = blockIdx.x * blockDim.x + threadIdx.x;
+  if (p >= P) return;
+  int bx = 0, by = 0;
+  if (prev) {
+    bx = 2 * prev[p * prev_stride];
+    by = 2 * prev[p * prev_stride + 1];
+  } else if (base) {
+    bx = base[2 * p];
+    by = base[2 * p + 1];
+  }
+  const unsigned long long* e = errs + p * errs_stride;
+  int best = 0;
+  unsigned long long be = 0;
+  int bd = 0;
+  for (int i = 0; i < 9; ++i) {
+    const int d = abs(i % 3 - 1) + abs(i / 3 - 1);
+    if (i == 0 || key_less(e[i], d, i, be, bd, best)) { best = i; be = e[i]; bd = d; }
+  }
+  acc[p * acc_stride] = bx + best % 3 - 1;
+  acc[p * acc_stride + 1] = by + best / 3 - 1;
 }
 
 }  // namespace mtb
@@ -387,10 +423,60 @@ extern "C" int mtb_find_offset_batch(const uint64_t* const* maps, const int32_t*
     a.errs_stride = 9 * n_levels;
     a.done = done + k;
     a.done_stride = n_levels;
+    a.a_row0 = 0;
+    a.a_rows = a.h;
+    a.b_row0 = 0;
+    a.b_rows = a.h;
+    a.decide = 1;
     a.tiles_x = (a.nw32 + kSTWords - 1) / kSTWords;
     const int tiles_y = (a.h + kSTRows - 1) / kSTRows;
     level_search_kernel<<<dim3(a.tiles_x * tiles_y, P), kSTThreads, 0, st>>>(a);
     ++launches;
   }
   return check_launch("level_search_kernel", launches);
+}
+
+extern "C" int mtb_search_level_rows(const uint64_t* const* maps, int w, int h, int64_t nwords64, int a_row0,
+                                     int a_rows, int b_row0, int b_rows, int P, const int32_t* prev,
+                                     int64_t prev_stride, const int32_t* base, unsigned long long* errs,
+                                     int64_t errs_stride, void* stream) {
+  clear_error();
+  MTB_REQUIRE(maps && errs, "null pointer");
+  MTB_REQUIRE(P >= 1 && P <= 65535, "pair count out of range");
+  MTB_REQUIRE(w >= 1 && h >= 1 && nwords64 * 64 >= w, "bad level dimensions");
+  MTB_REQUIRE(a_rows >= 0 && b_rows >= 0 && a_row0 >= 0 && a_row0 + a_rows <= h, "bad row windows");
+  cudaStream_t st = as_stream(stream);
+  for (int p = 0; p < P; ++p)
+    MTB_CUDA(cudaMemsetAsync(errs + p * errs_stride, 0, 9 * sizeof(unsigned long long), st));
+  if (a_rows == 0) return MTB_OK;
+  LevelSearchArgs a{};
+  a.maps = maps;
+  a.w = w;
+  a.h = h;
+  a.nw32 = (int)(2 * nwords64);
+  a.prev = prev;
+  a.prev_stride = prev_stride;
+  a.base = base;
+  a.errs = errs;
+  a.errs_stride = errs_stride;
+  a.a_row0 = a_row0;
+  a.a_rows = a_rows;
+  a.b_row0 = b_row0;
+  a.b_rows = b_rows;
+  a.decide = 0;
+  a.tiles_x = (a.nw32 + kSTWords - 1) / kSTWords;
+  const int tiles_y = (a_rows + kSTRows - 1) / kSTRows;
+  level_search_kernel<<<dim3(a.tiles_x * tiles_y, P), kSTThreads, 0, st>>>(a);
+  return check_launch("level_search_kernel");
+}
+
+extern "C" int mtb_decide_level(const unsigned long long* errs, int64_t errs_stride, const int32_t* prev,
+                                int64_t prev_stride, const int32_t* base, int32_t* acc, int64_t acc_stride, int P,
+                                void* stream) {
+  clear_error();
+  MTB_REQUIRE(errs && acc, "null pointer");
+  MTB_REQUIRE(P >= 1, "pair count out of range");
+  decide_level_kernel<<<(P + 127) / 128, 128, 0, as_stream(stream)>>>(errs, errs_stride, prev, prev_stride, base, acc,
+                                                                    acc_stride, P);
+  return check_launch("decide_level_kernel");
 }
