@@ -15,7 +15,7 @@ import threading
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "_lib", "libmtbalign_b200.so")
+LIB_PATH = os.environ.get("MTB_LIB_PATH") or os.path.join(_HERE, "_lib", "libmtbalign_b200.so")
 
 MAX_LEVELS = 16
 

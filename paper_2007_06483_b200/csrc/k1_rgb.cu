@@ -5,25 +5,27 @@
 // pyramid.py:17-62, threshold.py:25-28).  This kernel is the roofline kernel
 // of the whole path: it reads every RGB byte exactly once.  Design (sm_100a):
 //
-//  * One 1024-thread CTA per SM, persistent over a contiguous band of the
-//    interior 32x128-pixel tiles of one image (edge tiles go to the generic
-//    kernel in pyramid.cu).  Eight independent 128-thread groups each own one
-//    tile at a time and synchronise only on their own named barrier.
-//  * Each thread owns a 32-pixel row segment (96 RGB bytes).  The bytes of its
-//    NEXT tile are fetched with cp.async (LDGSTS, 16 B each, L2 evict-first
-//    policy) into the thread's own shared-memory slot right after it has
-//    pulled the current ones into registers, so the copy has a whole tile of
-//    work to land and no register holds in-flight data (32 warps/SM fit).
-//  * Gray via IDP.4A: pixel groups of 4 (12 bytes = 3 words) need 6 dp4a and
-//    3 byte-permutes; no byte extraction.
-//  * Levels 1-2 by all threads with SIMD pair sums in 16-bit lanes;
-//    levels 3-5 by one warp per tile (rotating) with warp syncs only.
-//  * Histograms: shared-memory atomics (ATOMS.POPC.INC aggregates equal
-//    addresses in a warp), reduced across a thread-block cluster through
-//    distributed shared memory, then one global RED per nonzero bin per
-//    cluster into a 128-B-strided ("spread") histogram.
-//  * Gray levels are stored with an L2::evict_last policy: the threshold pass
-//    re-reads them right after, ideally from L2.
+//  * One 512-thread CTA per SM, persistent over a contiguous band of the
+//    32x256-pixel tiles of one image.  Four independent 128-thread groups
+//    each own one tile at a time and synchronise only on their own named
+//    barrier; each group streams its tiles through a 2-stage ring with ONE
+//    TMA tensor copy per tile (24 KB, L2 evict-first: RGB is read once).
+//  * A thread owns an 8x8 pixel block: it pulls its 192 RGB bytes into
+//    registers first (24 conflict-free LDS.64), the group barrier frees the
+//    ring stage and the refill is issued before any arithmetic, so each TMA
+//    has a whole tile of work (about 2 tile-times) to land.
+//  * Gray via IDP.4A: 4 pixels (12 bytes = 3 words) cost 6 dp4a + 3 byte
+//    permutes.  Levels 1-3 of the block are thread-local (4x4, 2x2, 1x1;
+//    box sums by dp4a), levels 4-5 of the tile by one rotating warp from a
+//    128-byte level-3 buffer.
+//  * Histograms: shared-memory atomics (ATOMS.POPC.INC aggregates equal bins
+//    in a warp).  Each level's 1 KB histogram sits at a 1 KB-aligned shared
+//    address, so a bin address is ONE LOP3 (base | (sum >> 6 & 0x3fc)) after
+//    the shift.  CTA histograms are reduced across a thread-block cluster
+//    through DSMEM, then one global RED per nonzero bin per cluster into a
+//    128-B-strided ("spread") histogram.
+//  * Gray levels are stored with an optional L2::evict_last policy so a
+//    threshold pass that follows closely re-reads them from L2.
 #include <cooperative_groups.h>
 #include <cuda.h>
 #include <cudaTypedefs.h>
@@ -37,9 +39,14 @@ namespace cg = cooperative_groups;
 
 namespace mtb {
 
-constexpr int kK1Groups = 8;
+constexpr int kK1Groups = 4;
 constexpr int kK1GroupThreads = 128;
 constexpr int kK1Threads = kK1Groups * kK1GroupThreads;
+constexpr int kK1Stages = 2;
+constexpr int kK1TileRows = 32;
+constexpr int kK1TilePx = 256;
+constexpr int kK1RowBytes = 3 * kK1TilePx;                 // 768
+constexpr int kK1TileBytes = kK1TileRows * kK1RowBytes;    // 24 KB
 constexpr int kHistStrideK1 = 32;   // must equal kHistStride in pyramid.cu
 
 struct K1Args {
@@ -48,28 +55,24 @@ struct K1Args {
   int w, h;
   uint8_t* gray;
   int64_t gray_img_stride;
-  int64_t off[6], pitch[6];
+  int off[6], pitch[6];     // within-image byte offsets (image gray arena < 2 GB)
   int lw[6], lh[6];
   int nl;                 // levels produced (1..6)
   uint32_t* hist;         // spread histograms [img][level][bin * 32]
   int64_t hist_img_stride;
-  int tiles_x, tiles_y;   // ceil(w/128) x ceil(h/32)
-  int cluster;            // CTAs per cluster (1, 2, 4)
-  int probe;              // diagnostics only (MTB_K1_PROBE): 1 = stream tiles, skip all compute
-};
-
-constexpr int kTileRgbBytes = 32 * 384;   // one 32x128 tile of RGB8
-
-struct alignas(128) GroupSmem {
-  uint8_t rgb[2][kTileRgbBytes];  // TMA ring: two tiles in flight per group
-  uint8_t l3[2][4 * 16];          // level-3 values, double-buffered by tile parity
-  uint8_t l4[2 * 8];
-  unsigned long long full[2];     // mbarriers of the two ring stages
+  int tiles_x, tiles_y;   // ceil(w/256) x ceil(h/32)
+  int n_img;              // images of this launch (tiles are numbered image-major)
+  int keep_gray;          // store gray with L2::evict_last (else evict_normal)
+  int probe;              // diagnostics (MTB_K1_PROBE): 1 = stream tiles only, 2 = compute only (no TMA)
 };
 
 struct K1Smem {
-  GroupSmem grp[kK1Groups];
+  uint32_t hist[kK1Groups][6][256];                    // first: 1 KB-aligned levels, one set per group
+  uint8_t rgb[kK1Groups][kK1Stages][kK1TileBytes];     // TMA rings
+  uint8_t l3[kK1Groups][2][4][32];                     // level-3 tile values, by tile parity
+  unsigned long long full[kK1Groups][kK1Stages];       // mbarriers of the ring stages
 };
+constexpr int kK1SmemBytes = (int)sizeof(K1Smem) + 1024;  // + alignment slack
 
 __device__ __forceinline__ uint32_t smem_addr(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
 __device__ __forceinline__ void mbar_init(unsigned long long* bar, uint32_t count) {
@@ -90,33 +93,40 @@ __device__ __forceinline__ void mbar_wait(unsigned long long* bar, uint32_t pari
       "r"(parity)
       : "memory");
 }
-// TMA 3-D tile copy (box 96 u32 x 32 rows x 1 image) -> this CTA's smem.
+// TMA 3-D tile copy (box 192 u32 x 32 rows x 1 image) -> this CTA's smem.
 __device__ __forceinline__ void tma_tile(void* dst, const CUtensorMap* map, int c0, int c1, int c2,
-                                         unsigned long long* bar) {
+                                         unsigned long long* bar, uint64_t policy) {
   asm volatile(
-      "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], "
-      "[%5];" ::"r"(smem_addr(dst)),
-      "l"(map), "r"(c0), "r"(c1), "r"(c2), "r"(smem_addr(bar))
+      "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes.L2::cache_hint"
+      " [%0], [%1, {%2, %3, %4}], [%5], %6;" ::"r"(smem_addr(dst)),
+      "l"(map), "r"(c0), "r"(c1), "r"(c2), "r"(smem_addr(bar)), "l"(policy)
       : "memory");
-}
-// Bulk (TMA engine) copy of `bytes` contiguous bytes global -> this CTA's smem,
-// completing on `bar` (tx count).
-__device__ __forceinline__ void bulk_copy(void* dst, const void* src, uint32_t bytes, unsigned long long* bar) {
-  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-                   smem_addr(dst)),
-               "l"(src), "r"(bytes), "r"(smem_addr(bar))
-               : "memory");
-}
-
-__device__ __forceinline__ uint4 ld_stream16(const void* p) {
-  uint4 r;
-  asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
-               : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
-               : "l"(p));
-  return r;
 }
 __device__ __forceinline__ void group_bar(int g) {
   asm volatile("bar.sync %0, %1;" ::"r"(g + 1), "r"(kK1GroupThreads) : "memory");
+}
+// One histogram increment at a shared address (ATOMS.POPC.INC).
+#ifndef K1_EXP_NO_HIST
+__device__ __forceinline__ void hinc(uint32_t addr) { asm volatile("red.shared.add.u32 [%0], 1;" ::"r"(addr) : "memory"); }
+#else
+__device__ __forceinline__ void hinc(uint32_t addr) { asm volatile("" ::"r"(addr)); }
+#endif
+
+// Gray stores with an L2 policy (evict_last when a threshold pass follows).
+__device__ __forceinline__ void st_gray8(uint8_t* p, uint32_t a, uint32_t b, uint64_t policy) {
+#ifdef K1_EXP_NO_STORE
+  asm volatile("" ::"l"(p), "r"(a), "r"(b)); return;
+#endif
+  asm volatile("st.global.L2::cache_hint.v2.u32 [%0], {%1, %2}, %3;" ::"l"(p), "r"(a), "r"(b), "l"(policy) : "memory");
+}
+__device__ __forceinline__ void st_gray4(uint8_t* p, uint32_t a, uint64_t policy) {
+  asm volatile("st.global.L2::cache_hint.u32 [%0], %1, %2;" ::"l"(p), "r"(a), "l"(policy) : "memory");
+}
+__device__ __forceinline__ void st_gray2(uint8_t* p, uint32_t a, uint64_t policy) {
+  asm volatile("st.global.L2::cache_hint.u16 [%0], %1, %2;" ::"l"(p), "h"((unsigned short)a), "l"(policy) : "memory");
+}
+__device__ __forceinline__ void st_gray1(uint8_t* p, uint32_t a, uint64_t policy) {
+  asm volatile("st.global.L2::cache_hint.u8 [%0], %1, %2;" ::"l"(p), "h"((unsigned short)a), "l"(policy) : "memory");
 }
 
 // Four gray values (dp4a sums, gray = byte 1) of the 4 pixels in words w0..w2
@@ -130,14 +140,6 @@ __device__ __forceinline__ uint32_t gray4(uint32_t w0, uint32_t w1, uint32_t w2,
   const uint32_t g23 = __byte_perm(s[2], s[3], 0x0051);
   return __byte_perm(g01, g23, 0x5410);
 }
-
-// Two 2x2 box averages from one word of each of two rows (4 source pixels
-// per word): avg of bytes 0-1 in byte 0, avg of bytes 2-3 in byte 2.
-__device__ __forceinline__ uint32_t box2(uint32_t u, uint32_t d) {
-  const uint32_t s = (u & 0x00FF00FFu) + ((u >> 8) & 0x00FF00FFu) + (d & 0x00FF00FFu) + ((d >> 8) & 0x00FF00FFu) +
-                     0x00020002u;
-  return s >> 2;
-}
 // 2x2 box sum + 2 of the byte pair `pair` (0: bytes 0-1, 1: bytes 2-3) of a
 // word of the upper row u and of the lower row d: (a+b+c+d+2), < 1024.  The
 // average is sum >> 2 and its histogram byte offset is sum & 0x3fc.
@@ -145,247 +147,230 @@ __device__ __forceinline__ uint32_t box_sum(uint32_t u, uint32_t d, int pair) {
   const uint32_t w = pair ? 0x01010000u : 0x00000101u;
   return __dp4a(u, w, __dp4a(d, w, 2u));
 }
-// Four box sums -> four packed average bytes.
-__device__ __forceinline__ uint32_t pack_sums(uint32_t s0, uint32_t s1, uint32_t s2, uint32_t s3) {
-  const uint32_t x01 = (s0 + (s1 << 16)) >> 2, x23 = (s2 + (s3 << 16)) >> 2;
-  return __byte_perm(x01, x23, 0x6420);
-}
-// Increment the counter at byte offset `off` of the (static) histogram array;
-// written as plain C++ on the array so the base folds into the ATOMS address.
-__device__ __forceinline__ void hist_inc(uint32_t* hist, uint32_t off) { atomicAdd(&hist[off >> 2], 1u); }
-// Pack the two results of two box2 words into 4 consecutive bytes.
-__device__ __forceinline__ uint32_t pack_box(uint32_t q0, uint32_t q1) { return __byte_perm(q0, q1, 0x6420); }
 
-// Thread layout inside a 128-thread group (one 32x128 tile): thread = (ry, cx)
-// owns level-0 rows 2ry, 2ry+1 and columns 16cx .. 16cx+15 (ry 0..15, cx 0..7);
-// lane = (ry & 3) * 8 + cx, warp-in-group = ry >> 2.  Level 1 is computed in
-// registers, level 2 with one shuffle (partner ry^1 = lane^8), level 3 with
-// another (partner ry^2 = lane^16); levels 4-5 (which span warps) go through a
-// 64-byte shared buffer and one named barrier per tile.
-// CLUSTER: reduce histograms across a thread-block cluster through DSMEM.  A
-// separate instantiation, because cluster-capable code addresses its own
-// shared memory through the CTA's cluster window (an extra add per access).
-template <bool CLUSTER>
+// One 32x256 tile of one group; this thread's 8x8 block starts at tile row
+// 8*wg, tile column 8*lane.  v = its RGB bytes (row r: words v[r][0..2]).
+template <bool FULL>
+__device__ __forceinline__ void k1_block(const K1Args& a, uint8_t* gray, const uint2 (&v)[8][3], int tx, int ty,
+                                         int wg, int lane, uint32_t hb, uint64_t policy, uint8_t* l3_slot) {
+  const int x0 = tx * kK1TilePx + 8 * lane;
+  const int y0 = ty * kK1TileRows + 8 * wg;
+  // ---- level 0 (8 rows x 8 px) and level 1 (4 rows x 4 px) ---------------
+  uint32_t l1[4];
+  {
+    uint8_t* p0 = gray + (a.off[0] + y0 * a.pitch[0] + x0);
+    uint8_t* p1 = gray + (a.off[1] + (y0 >> 1) * a.pitch[1] + (x0 >> 1));
+    const bool col0 = FULL || x0 < a.pitch[0];
+    const int nv0 = FULL ? 8 : min(8, max(0, a.w - x0));
+    const int x1 = x0 >> 1;
+    const int nv1 = FULL ? 4 : min(4, max(0, a.lw[1] - x1));
+#pragma unroll
+    for (int rp = 0; rp < 4; ++rp) {
+      uint32_t gw[2][2];
+#pragma unroll
+      for (int j = 0; j < 2; ++j) {
+        const int r = 2 * rp + j;
+        const bool row_ok = FULL || (y0 + r < a.h);
+        uint32_t sa[4], sb[4];
+        gw[j][0] = gray4(v[r][0].x, v[r][0].y, v[r][1].x, sa);
+        gw[j][1] = gray4(v[r][1].y, v[r][2].x, v[r][2].y, sb);
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          if (FULL || (row_ok && i < nv0)) hinc(hb | ((sa[i] >> 6) & 0x3fcu));
+          if (FULL || (row_ok && 4 + i < nv0)) hinc(hb | ((sb[i] >> 6) & 0x3fcu));
+        }
+        if (row_ok && col0) st_gray8(p0 + r * a.pitch[0], gw[j][0], gw[j][1], policy);
+      }
+      if (a.nl >= 2) {
+        const uint32_t s0 = box_sum(gw[0][0], gw[1][0], 0), s1 = box_sum(gw[0][0], gw[1][0], 1);
+        const uint32_t s2 = box_sum(gw[0][1], gw[1][1], 0), s3 = box_sum(gw[0][1], gw[1][1], 1);
+        const uint32_t hb1 = hb + 1024;
+        const bool row_ok = FULL || ((y0 >> 1) + rp < a.lh[1]);
+        if (FULL || (row_ok && 0 < nv1)) hinc(hb1 | (s0 & 0x3fcu));
+        if (FULL || (row_ok && 1 < nv1)) hinc(hb1 | (s1 & 0x3fcu));
+        if (FULL || (row_ok && 2 < nv1)) hinc(hb1 | (s2 & 0x3fcu));
+        if (FULL || (row_ok && 3 < nv1)) hinc(hb1 | (s3 & 0x3fcu));
+        const uint32_t x01 = (s0 + (s1 << 16)) >> 2, x23 = (s2 + (s3 << 16)) >> 2;
+        l1[rp] = __byte_perm(x01, x23, 0x6420);
+        if (row_ok && (FULL || x1 < a.pitch[1])) st_gray4(p1 + rp * a.pitch[1], l1[rp], policy);
+      }
+    }
+  }
+  if (a.nl < 3) return;
+  // ---- level 2 (2 rows x 2 px) --------------------------------------------
+  uint32_t l2[2];
+  {
+    const int x2 = x0 >> 2, y2 = y0 >> 2;
+    const int nv2 = FULL ? 2 : min(2, max(0, a.lw[2] - x2));
+    uint8_t* p2 = gray + (a.off[2] + y2 * a.pitch[2] + x2);
+    const uint32_t hb2 = hb + 2048;
+#pragma unroll
+    for (int r = 0; r < 2; ++r) {
+      const uint32_t s0 = box_sum(l1[2 * r], l1[2 * r + 1], 0), s1 = box_sum(l1[2 * r], l1[2 * r + 1], 1);
+      const bool row_ok = FULL || (y2 + r < a.lh[2]);
+      if (FULL || (row_ok && 0 < nv2)) hinc(hb2 | (s0 & 0x3fcu));
+      if (FULL || (row_ok && 1 < nv2)) hinc(hb2 | (s1 & 0x3fcu));
+      l2[r] = ((s0 >> 2) & 0xffu) | ((s1 << 6) & 0xff00u);
+      if (row_ok && (FULL || x2 < a.pitch[2])) st_gray2(p2 + r * a.pitch[2], l2[r], policy);
+    }
+  }
+  if (a.nl < 4) return;
+  // ---- level 3 (1 px) -----------------------------------------------------
+  {
+    const int x3 = x0 >> 3, y3 = y0 >> 3;
+    const uint32_t s = box_sum(l2[0], l2[1], 0);
+    const uint32_t v3 = s >> 2;
+    *l3_slot = (uint8_t)v3;
+    if (FULL || (x3 < a.lw[3] && y3 < a.lh[3])) {
+      hinc((hb + 3072) | (s & 0x3fcu));
+      st_gray1(gray + (a.off[3] + y3 * a.pitch[3] + x3), v3, policy);
+    }
+  }
+}
+
+// Levels 4 (2 x 16 px) and 5 (1 x 8 px) of tile (tx, ty) from its level-3
+// values l3[4][32]; executed by one whole warp.
+__device__ __forceinline__ void k1_levels45(const K1Args& a, uint8_t* gray, const uint8_t (*l3)[32], int tx, int ty,
+                                            int lane, uint32_t hb, bool full, uint64_t policy) {
+  const int r = lane >> 4, c = lane & 15;
+  const uint32_t v4 = (l3[2 * r][2 * c] + l3[2 * r][2 * c + 1] + l3[2 * r + 1][2 * c] + l3[2 * r + 1][2 * c + 1] + 2u) >> 2;
+  {
+    const int y = ty * 2 + r, x = tx * 16 + c;
+    if (full || (y < a.lh[4] && x < a.lw[4])) {
+      st_gray1(gray + (a.off[4] + y * a.pitch[4] + x), v4, policy);
+      hinc((hb + 4096) | (v4 << 2));
+    }
+  }
+  if (a.nl < 6) return;
+  const int c5 = lane & 7;
+  const uint32_t q0 = __shfl_sync(0xffffffffu, v4, 2 * c5), q1 = __shfl_sync(0xffffffffu, v4, 2 * c5 + 1);
+  const uint32_t q2 = __shfl_sync(0xffffffffu, v4, 16 + 2 * c5), q3 = __shfl_sync(0xffffffffu, v4, 17 + 2 * c5);
+  if (lane < 8) {
+    const uint32_t v5 = (q0 + q1 + q2 + q3 + 2u) >> 2;
+    const int y = ty, x = tx * 8 + lane;
+    if (full || (y < a.lh[5] && x < a.lw[5])) {
+      st_gray1(gray + (a.off[5] + y * a.pitch[5] + x), v5, policy);
+      hinc((hb + 5120) | (v5 << 2));
+    }
+  }
+}
+
 __global__ void __launch_bounds__(kK1Threads, 1) k1_rgb_pyramid_kernel(K1Args a, const __grid_constant__ CUtensorMap rgb_map) {
   extern __shared__ __align__(128) uint8_t k1_smem_raw[];
-  K1Smem& SM = *reinterpret_cast<K1Smem*>(k1_smem_raw);
-  __shared__ uint32_t s_hist[6 * 256];   // static: its base folds into the ATOMS immediate
+  const uint32_t raw = smem_addr(k1_smem_raw);
+  K1Smem& S = *reinterpret_cast<K1Smem*>(k1_smem_raw + ((1024u - (raw & 1023u)) & 1023u));
 
   const int tid = threadIdx.x;
   const int g = tid >> 7;             // group
   const int t = tid & 127;            // thread in group
   const int lane = tid & 31;
-  const int wig = t >> 5;             // warp in group
-  const int cx = lane & 7;
-  const int ry = (wig << 2) | (lane >> 3);
-  const int img = blockIdx.y;
-  GroupSmem& S = SM.grp[g];
+  const int wg = t >> 5;              // warp in group: tile rows 8wg..8wg+7
+  // This group's histograms: level k at hb + 1024 k (1 KB aligned, so a bin
+  // address is hb_k | 4*bin).
+  uint32_t* gh_s = &S.hist[g][0][0];
+  const uint32_t hb = smem_addr(gh_s);
 
-  for (int i = tid; i < 6 * 256; i += kK1Threads) s_hist[i] = 0;
+  for (int i = t; i < 6 * 256; i += kK1GroupThreads) gh_s[i] = 0;
   if (t == 0) {
-    mbar_init(&S.full[0], 1);
-    mbar_init(&S.full[1], 1);
+    for (int s = 0; s < kK1Stages; ++s) mbar_init(&S.full[g][s], 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncthreads();
 
-  const uint8_t* rgb = a.rgb + img * a.rgb_img_stride;
-  uint8_t* gray = a.gray + img * a.gray_img_stride;
+  uint64_t pol_first, pol_gray;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol_first));
+  if (a.keep_gray)
+    asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol_gray));
+  else
+    asm volatile("createpolicy.fractional.L2::evict_normal.b64 %0, 1.0;" : "=l"(pol_gray));
 
-  const int ntiles = a.tiles_x * a.tiles_y;
+  // Tiles are numbered image-major over the whole launch; this CTA owns a
+  // contiguous range and its group g every 4th tile of it.
+  const int tiles_img = a.tiles_x * a.tiles_y;
+  const int64_t ntiles = (int64_t)tiles_img * a.n_img;
   const int t_begin = (int)((int64_t)blockIdx.x * ntiles / gridDim.x);
   const int t_end = (int)((int64_t)(blockIdx.x + 1) * ntiles / gridDim.x);
 
-  // One thread per group streams tiles into the group's 2-stage ring with a
-  // single TMA tensor copy each (box = the tile's 32 rows x 384 bytes).
+  auto coords = [&](int tile, int& img, int& ty, int& tx) {
+    img = tile / tiles_img;
+    const int r = tile - img * tiles_img;
+    ty = r / a.tiles_x;
+    tx = r - ty * a.tiles_x;
+  };
   auto issue = [&](int tile, int stage) {
-    if (t == 0) {
-      const int ty = tile / a.tiles_x, tx = tile - ty * a.tiles_x;
-      mbar_expect_tx(&S.full[stage], kTileRgbBytes);
-      tma_tile(S.rgb[stage], &rgb_map, 96 * tx, 32 * ty, img, &S.full[stage]);
+    int img, ty, tx;
+    coords(tile, img, ty, tx);
+    mbar_expect_tx(&S.full[g][stage], kK1TileBytes);
+    tma_tile(S.rgb[g][stage], &rgb_map, (kK1RowBytes / 4) * tx, kK1TileRows * ty, img, &S.full[g][stage], pol_first);
+  };
+  // Flush this group's histograms of image `img` to the global spread
+  // histograms and zero them (called by the whole group after a group barrier).
+  auto flush = [&](int img) {
+    uint32_t* gh = a.hist + img * a.hist_img_stride;
+    for (int i = t; i < a.nl * 256; i += kK1GroupThreads) {
+      const uint32_t c = gh_s[i];
+      if (c) {
+        atomicAdd(&gh[(int64_t)i * kHistStrideK1], c);
+        gh_s[i] = 0;
+      }
     }
   };
-  if (t_begin + g < t_end) issue(t_begin + g, 0);
-  if (t_begin + g + kK1Groups < t_end) issue(t_begin + g + kK1Groups, 1);
-
-  int iter = 0;
-  int ty = (t_begin + g) / a.tiles_x, tx = (t_begin + g) - ty * a.tiles_x;
-  for (int tile = t_begin + g; tile < t_end; tile += kK1Groups, ++iter) {
-    if (iter) {  // advance (ty, tx) by kK1Groups tiles without a division
-      tx += kK1Groups;
-      while (tx >= a.tiles_x) { tx -= a.tiles_x; ++ty; }
-    }
-    const int y0 = ty * 32 + 2 * ry, x0 = tx * 128 + 16 * cx;
-    const int stage = iter & 1;
-    // Interior tiles need no bounds checks; edge tiles (TMA zero-fills what
-    // lies outside the image) mask their histogram counts and row stores.
-    const bool full = (ty * 32 + 32 <= a.h) && (tx * 128 + 128 <= a.w);
-
-    auto body = [&](auto full_tag) {
-      constexpr bool FULL = decltype(full_tag)::value;
-      // ---- level 0: 2 rows x 16 pixels ------------------------------------
-      uint32_t gw[2][4];
-      {
-        mbar_wait(&S.full[stage], (iter >> 1) & 1);
-        const uint8_t* p0 = S.rgb[stage] + (2 * ry) * 384 + 48 * cx;
-        const uint8_t* p1 = p0 + 384;
-        const uint4 q0 = *reinterpret_cast<const uint4*>(p0), q1 = *reinterpret_cast<const uint4*>(p0 + 16),
-                    q2 = *reinterpret_cast<const uint4*>(p0 + 32);
-        const uint4 q3 = *reinterpret_cast<const uint4*>(p1), q4 = *reinterpret_cast<const uint4*>(p1 + 16),
-                    q5 = *reinterpret_cast<const uint4*>(p1 + 32);
-        const uint32_t wv[2][12] = {{q0.x, q0.y, q0.z, q0.w, q1.x, q1.y, q1.z, q1.w, q2.x, q2.y, q2.z, q2.w},
-                                    {q3.x, q3.y, q3.z, q3.w, q4.x, q4.y, q4.z, q4.w, q5.x, q5.y, q5.z, q5.w}};
-        const int nvx = FULL ? 16 : min(16, max(0, a.w - x0));
-#pragma unroll
-        for (int j = 0; j < 2; ++j) {
-          const bool row_ok = FULL || (y0 + j < a.h);
-#pragma unroll
-          for (int k = 0; k < 4; ++k) {
-            uint32_t s4[4];
-            gw[j][k] = gray4(wv[j][3 * k], wv[j][3 * k + 1], wv[j][3 * k + 2], s4);
-#pragma unroll
-            for (int i = 0; i < 4; ++i) {
-              // 256 bins: byte offset 4*(s>>8).  (A 16K-sub-bin variant with a
-              // one-op address measured slower: fewer equal addresses per warp
-              // for ATOMS.POPC.INC to aggregate.)
-              if (FULL) {
-                hist_inc(s_hist, (s4[i] >> 6) & 0x3fcu);
-              } else if (row_ok && 4 * k + i < nvx) {
-                hist_inc(s_hist, (s4[i] >> 6) & 0x3fcu);
-              }
-            }
-          }
-          if (row_ok)
-            *reinterpret_cast<uint4*>(gray + a.off[0] + (int64_t)(y0 + j) * a.pitch[0] + x0) =
-                make_uint4(gw[j][0], gw[j][1], gw[j][2], gw[j][3]);
-        }
-      }
-      if (a.nl < 2) return;
-
-      // ---- level 1: 1 row x 8 pixels, in registers ------------------------
-      uint32_t l1[2];
-      {
-        uint32_t sm[8];
-#pragma unroll
-        for (int i = 0; i < 8; ++i) sm[i] = box_sum(gw[0][i >> 1], gw[1][i >> 1], i & 1);
-        l1[0] = pack_sums(sm[0], sm[1], sm[2], sm[3]);
-        l1[1] = pack_sums(sm[4], sm[5], sm[6], sm[7]);
-        const int y = ty * 16 + ry, x = tx * 64 + 8 * cx;
-        if (FULL || y < a.lh[1]) {
-          *reinterpret_cast<uint2*>(gray + a.off[1] + (int64_t)y * a.pitch[1] + x) = make_uint2(l1[0], l1[1]);
-          const int nv = FULL ? 8 : min(8, max(0, a.lw[1] - x));
-#pragma unroll
-          for (int i = 0; i < 8; ++i) {
-            if (FULL || i < nv) hist_inc(s_hist + 256, sm[i] & 0x3fcu);
-          }
-        }
-      }
-      if (a.nl < 3) return;
-
-      // ---- level 2: partner ry^1 (lane^8); even-ry thread emits 4 pixels --
-      uint32_t l2 = 0;
-      {
-        const uint32_t o0 = __shfl_xor_sync(0xffffffffu, l1[0], 8);
-        const uint32_t o1 = __shfl_xor_sync(0xffffffffu, l1[1], 8);
-        if ((ry & 1) == 0) {
-          const uint32_t s0 = box_sum(l1[0], o0, 0), s1 = box_sum(l1[0], o0, 1);
-          const uint32_t s2 = box_sum(l1[1], o1, 0), s3 = box_sum(l1[1], o1, 1);
-          l2 = pack_sums(s0, s1, s2, s3);
-          const int y = ty * 8 + (ry >> 1), x = tx * 32 + 4 * cx;
-          if (FULL || y < a.lh[2]) {
-            *reinterpret_cast<uint32_t*>(gray + a.off[2] + (int64_t)y * a.pitch[2] + x) = l2;
-            const int nv = FULL ? 4 : min(4, max(0, a.lw[2] - x));
-            if (FULL || 0 < nv) hist_inc(s_hist + 512, s0 & 0x3fcu);
-            if (FULL || 1 < nv) hist_inc(s_hist + 512, s1 & 0x3fcu);
-            if (FULL || 2 < nv) hist_inc(s_hist + 512, s2 & 0x3fcu);
-            if (FULL || 3 < nv) hist_inc(s_hist + 512, s3 & 0x3fcu);
-          }
-        }
-      }
-      if (a.nl < 4) return;
-
-      // ---- level 3: partner ry^2 (lane^16); ry%4==0 thread emits 2 pixels -
-      {
-        const uint32_t o = __shfl_xor_sync(0xffffffffu, l2, 16);
-        if ((ry & 3) == 0) {
-          const uint32_t s0 = box_sum(l2, o, 0), s1 = box_sum(l2, o, 1);
-          const uint32_t v0 = s0 >> 2, v1 = s1 >> 2;
-          const uint16_t pk = (uint16_t)(v0 | (v1 << 8));
-          const int r3 = ry >> 2;  // 0..3
-          *reinterpret_cast<uint16_t*>(&S.l3[iter & 1][r3 * 16 + 2 * cx]) = pk;
-          const int y = ty * 4 + r3, x = tx * 16 + 2 * cx;
-          if (FULL || y < a.lh[3]) {
-            *reinterpret_cast<uint16_t*>(gray + a.off[3] + (int64_t)y * a.pitch[3] + x) = pk;
-            if (FULL || x < a.lw[3]) hist_inc(s_hist + 768, s0 & 0x3fcu);
-            if (FULL || x + 1 < a.lw[3]) hist_inc(s_hist + 768, s1 & 0x3fcu);
-          }
-        }
-      }
-    };
-    if (a.probe) {
-      mbar_wait(&S.full[stage], (iter >> 1) & 1);
-    } else if (full) {
-      body(std::true_type{});
-    } else {
-      body(std::false_type{});
-    }
-
-    group_bar(g);  // every thread has consumed ring stage `stage` (and written l3)
-    if (tile + 2 * kK1Groups < t_end) {
-      if (t == 0) asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-      issue(tile + 2 * kK1Groups, stage);
-    }
-    if (a.nl < 5) continue;
-
-    // ---- levels 4..5: one warp of the group (rotating) --------------------
-    if (wig == (iter & 3)) {
-      const uint8_t* l3 = S.l3[iter & 1];
-      if (lane < 16) {  // level 4: 2 x 8
-        const int r = lane >> 3, c = lane & 7;
-        const uint8_t* sp = l3 + (2 * r) * 16 + 2 * c;
-        const uint32_t v = (sp[0] + sp[1] + sp[16] + sp[17] + 2u) >> 2;
-        S.l4[r * 8 + c] = (uint8_t)v;
-        const int y = ty * 2 + r, x = tx * 8 + c;
-        if (full || (y < a.lh[4] && x < a.lw[4])) {
-          gray[a.off[4] + (int64_t)y * a.pitch[4] + x] = (uint8_t)v;
-          atomicAdd(&s_hist[1024 + v], 1u);
-        }
-      }
-      __syncwarp();
-      if (a.nl > 5 && lane < 4) {  // level 5: 1 x 4
-        const uint8_t* sp = S.l4 + 2 * lane;
-        const uint32_t v = (sp[0] + sp[1] + sp[8] + sp[9] + 2u) >> 2;
-        const int y = ty, x = tx * 4 + lane;
-        if (full || (y < a.lh[5] && x < a.lw[5])) {
-          gray[a.off[5] + (int64_t)y * a.pitch[5] + x] = (uint8_t)v;
-          atomicAdd(&s_hist[1280 + v], 1u);
-        }
-      }
-      __syncwarp();
-    }
+  if (t == 0 && a.probe != 2) {
+    for (int s = 0; s < kK1Stages; ++s)
+      if (t_begin + g + kK1Groups * s < t_end) issue(t_begin + g + kK1Groups * s, s);
   }
 
-  // ---- histogram reduction: CTA -> cluster leader (DSMEM) -> global -------
-  __syncthreads();
-
-  uint32_t* gh = a.hist + img * a.hist_img_stride;
-  const int nbins = a.nl * 256;
-  if constexpr (CLUSTER) {
-    cg::cluster_group cl = cg::this_cluster();
-    cl.sync();
-    if (cl.block_rank() != 0) {
-      uint32_t* dst = cl.map_shared_rank(s_hist, 0);
-      for (int i = tid; i < nbins; i += kK1Threads) {
-        const uint32_t v = s_hist[i];
-        if (v) atomicAdd(&dst[i], v);
-      }
+  int k = 0, pimg = -1, ptx = 0, pty = 0;
+  bool pfull = true;
+  uint8_t* gray = a.gray;
+  for (int tile = t_begin + g; tile < t_end; tile += kK1Groups, ++k) {
+    const int stage = k % kK1Stages;
+    int img, ty, tx;
+    coords(tile, img, ty, tx);
+    const bool full = (ty * kK1TileRows + kK1TileRows <= a.h) && (tx * kK1TilePx + kK1TilePx <= a.w);
+    // Pull this thread's 8x8-pixel RGB block into registers.
+    uint2 v[8][3];
+    if (a.probe != 2) mbar_wait(&S.full[g][stage], (uint32_t)(k / kK1Stages) & 1u);
+    {
+      const uint8_t* src = S.rgb[g][stage] + (8 * wg) * kK1RowBytes + 24 * lane;
+#pragma unroll
+      for (int r = 0; r < 8; ++r)
+#pragma unroll
+        for (int c = 0; c < 3; ++c) v[r][c] = *reinterpret_cast<const uint2*>(src + r * kK1RowBytes + 8 * c);
     }
-    cl.sync();
-    if (cl.block_rank() != 0) return;
+    group_bar(g);  // stage consumed by all 128 threads; l3 of tile k-1 complete
+    if (t == 0 && a.probe != 2 && tile + kK1Groups * kK1Stages < t_end) {
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      issue(tile + kK1Groups * kK1Stages, stage);
+    }
+    if (a.probe == 1) continue;
+    if (k > 0 && a.nl >= 5 && wg == ((k - 1) & 3))
+      k1_levels45(a, gray, S.l3[g][(k - 1) & 1], ptx, pty, lane, hb, pfull, pol_gray);
+    if (img != pimg) {
+      // First tile of a new image: the previous image's counts are complete
+      // in this group (its level-4/5 tail was just done above).
+      if (pimg >= 0) {
+        group_bar(g);
+        flush(pimg);
+        group_bar(g);
+      }
+      gray = a.gray + img * a.gray_img_stride;
+    }
+    uint8_t* l3_slot = &S.l3[g][k & 1][wg][lane];
+    if (full)
+      k1_block<true>(a, gray, v, tx, ty, wg, lane, hb, pol_gray, l3_slot);
+    else
+      k1_block<false>(a, gray, v, tx, ty, wg, lane, hb, pol_gray, l3_slot);
+    pimg = img;
+    ptx = tx;
+    pty = ty;
+    pfull = full;
   }
-  for (int i = tid; i < nbins; i += kK1Threads) {
-    const uint32_t v = s_hist[i];
-    if (v) atomicAdd(&gh[(int64_t)i * kHistStrideK1], v);
+  group_bar(g);
+  if (a.probe != 1 && k > 0) {
+    if (a.nl >= 5 && wg == ((k - 1) & 3)) k1_levels45(a, gray, S.l3[g][(k - 1) & 1], ptx, pty, lane, hb, pfull, pol_gray);
+    group_bar(g);
+    flush(pimg);
   }
 }
 
@@ -406,8 +391,11 @@ bool k1_rgb_supported(int w, int64_t rgb_pitch, int64_t rgb_img_stride, const vo
          ((uintptr_t)rgb & 15) == 0 && encode_tiled() != nullptr;
 }
 
-// Levels 0..min(n,6)-1 of the interior tiles of n_img images (chunks of <= 4
-// images per launch so every launch fills the GPU with one CTA per SM).
+static int g_keep_gray = 0;   // set by mtb_set_gray_policy (capi.cu)
+void k1_set_keep_gray(int v) { g_keep_gray = v; }
+
+// Levels 0..min(n,6)-1 of n_img images in ONE persistent launch (one CTA per
+// SM over the image-major tile sequence).
 int launch_k1_rgb(const uint8_t* rgb, int64_t rgb_pitch, int64_t rgb_img_stride, int n_img, const Plan& p,
                   uint8_t* gray, uint32_t* spread_hist, int64_t hist_img_stride, cudaStream_t st) {
   K1Args a{};
@@ -416,79 +404,60 @@ int launch_k1_rgb(const uint8_t* rgb, int64_t rgb_pitch, int64_t rgb_img_stride,
   a.w = p.lv[0].w;
   a.h = p.lv[0].h;
   a.gray_img_stride = p.gray_img_bytes;
+  if (p.gray_img_bytes >= ((int64_t)1 << 31)) {
+    set_error("k1: gray arena of one image exceeds 2 GB");
+    return MTB_EINVAL;
+  }
   a.nl = p.n < 6 ? p.n : 6;
   for (int k = 0; k < 6; ++k) {
     const int l = k < p.n ? k : p.n - 1;
-    a.off[k] = p.lv[l].gray_off;
-    a.pitch[k] = p.lv[l].gray_pitch;
+    a.off[k] = (int)p.lv[l].gray_off;
+    a.pitch[k] = (int)p.lv[l].gray_pitch;
     a.lw[k] = k < p.n ? p.lv[k].w : 0;
     a.lh[k] = k < p.n ? p.lv[k].h : 0;
   }
   a.hist_img_stride = hist_img_stride;
+  a.keep_gray = g_keep_gray;
   {
     const char* pr = getenv("MTB_K1_PROBE");
     a.probe = pr ? atoi(pr) : 0;
   }
-  a.tiles_x = (a.w + 127) / 128;   // edge tiles included: TMA zero-fills outside the image
-  a.tiles_y = (a.h + 31) / 32;
-  const int ntiles = a.tiles_x * a.tiles_y;
+  a.tiles_x = (a.w + kK1TilePx - 1) / kK1TilePx;   // edge tiles included: TMA zero-fills outside the image
+  a.tiles_y = (a.h + kK1TileRows - 1) / kK1TileRows;
+  a.n_img = n_img;
+  const int64_t ntiles = (int64_t)a.tiles_x * a.tiles_y * n_img;
   if (ntiles == 0) return MTB_OK;
+  if (ntiles >= ((int64_t)1 << 31)) {
+    set_error("k1: too many tiles in one launch");
+    return MTB_EINVAL;
+  }
   static bool attr_done = false;
-  const int smem = (int)sizeof(K1Smem);
   if (!attr_done) {
-    MTB_CUDA(cudaFuncSetAttribute(k1_rgb_pyramid_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-    MTB_CUDA(cudaFuncSetAttribute(k1_rgb_pyramid_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    MTB_CUDA(cudaFuncSetAttribute(k1_rgb_pyramid_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kK1SmemBytes));
     attr_done = true;
   }
-  const int sms = num_sms();
-  int launches = 0;
-  for (int i0 = 0; i0 < n_img; i0 += 4) {
-    const int c = n_img - i0 < 4 ? n_img - i0 : 4;
-    int x = sms / c;
-    if (x > (ntiles + kK1Groups - 1) / kK1Groups) x = (ntiles + kK1Groups - 1) / kK1Groups;
-    if (x < 1) x = 1;
-    int cl = 1;
-    if (x % 4 == 0) cl = 4;
-    else if (x % 2 == 0) cl = 2;
-    a.cluster = cl;
-    a.rgb = rgb + i0 * rgb_img_stride;
-    a.gray = gray + i0 * p.gray_img_bytes;
-    CUtensorMap map;
-    {
-      const cuuint64_t dims[3] = {(cuuint64_t)(3 * (int64_t)a.w / 4), (cuuint64_t)a.h, (cuuint64_t)c};
-      const cuuint64_t strides[2] = {(cuuint64_t)rgb_pitch, (cuuint64_t)rgb_img_stride};
-      const cuuint32_t box[3] = {96, 32, 1};
-      const cuuint32_t estr[3] = {1, 1, 1};
-      const CUresult r = encode_tiled()(&map, CU_TENSOR_MAP_DATA_TYPE_UINT32, 3, (void*)a.rgb, dims, strides, box,
-                                        estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
-                                        CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-      if (r != CUDA_SUCCESS) {
-        set_error("cuTensorMapEncodeTiled failed for the RGB batch");
-        return MTB_ECUDA;
-      }
-    }
-    a.hist = spread_hist + i0 * hist_img_stride;
-    cudaLaunchConfig_t cfg{};
-    cfg.gridDim = dim3((unsigned)x, (unsigned)c);
-    cfg.blockDim = dim3(kK1Threads);
-    cfg.dynamicSmemBytes = smem;
-    cfg.stream = st;
-    cudaLaunchAttribute attr[1];
-    attr[0].id = cudaLaunchAttributeClusterDimension;
-    attr[0].val.clusterDim.x = cl;
-    attr[0].val.clusterDim.y = 1;
-    attr[0].val.clusterDim.z = 1;
-    cfg.attrs = attr;
-    cfg.numAttrs = cl > 1 ? 1 : 0;
-    const cudaError_t e = cl > 1 ? cudaLaunchKernelEx(&cfg, k1_rgb_pyramid_kernel<true>, a, map)
-                                 : cudaLaunchKernelEx(&cfg, k1_rgb_pyramid_kernel<false>, a, map);
-    if (e != cudaSuccess) {
-      set_error(std::string("k1_rgb_pyramid_kernel: ") + cudaGetErrorString(e));
+  int x = num_sms();
+  if (x > (ntiles + kK1Groups - 1) / kK1Groups) x = (int)((ntiles + kK1Groups - 1) / kK1Groups);
+  if (x < 1) x = 1;
+  a.rgb = rgb;
+  a.gray = gray;
+  a.hist = spread_hist;
+  CUtensorMap map;
+  {
+    const cuuint64_t dims[3] = {(cuuint64_t)(3 * (int64_t)a.w / 4), (cuuint64_t)a.h, (cuuint64_t)n_img};
+    const cuuint64_t strides[2] = {(cuuint64_t)rgb_pitch, (cuuint64_t)rgb_img_stride};
+    const cuuint32_t box[3] = {kK1RowBytes / 4, kK1TileRows, 1};
+    const cuuint32_t estr[3] = {1, 1, 1};
+    const CUresult r = encode_tiled()(&map, CU_TENSOR_MAP_DATA_TYPE_UINT32, 3, (void*)rgb, dims, strides, box, estr,
+                                      CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                                      CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) {
+      set_error("cuTensorMapEncodeTiled failed for the RGB batch");
       return MTB_ECUDA;
     }
-    ++launches;
   }
-  return check_launch("k1_rgb_pyramid_kernel", launches);
+  k1_rgb_pyramid_kernel<<<x, kK1Threads, kK1SmemBytes, st>>>(a, map);
+  return check_launch("k1_rgb_pyramid_kernel");
 }
 
 }  // namespace mtb
