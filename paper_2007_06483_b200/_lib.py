@@ -58,6 +58,9 @@ SIGNATURES = {
     "mtb_threshold_levels_medians": [_c_void_p, _i32, _i32, _i32, _i32, _i32, _c_void_p, _c_void_p, _c_void_p,
                                      _i32, _c_void_p],
     "mtb_decide_level": [_c_void_p, _i64, _c_void_p, _i64, _c_void_p, _c_void_p, _i64, _i32, _c_void_p],
+    "mtb_align_fused": [_c_void_p, _i64, _i64, _i32, _i32, _i32, _i32, _i32, _c_void_p, _i32,
+                        _c_void_p, _c_void_p, _c_void_p, _c_void_p, _c_void_p, _c_void_p, _c_void_p, _c_void_p,
+                        _c_void_p, _c_void_p],
 }
 
 # Non-status entry points.
@@ -66,6 +69,7 @@ AUX_SIGNATURES = {
     "mtb_abi_version": ([], ctypes.c_int),
     "mtb_launch_count": ([], ctypes.c_uint64),
     "mtb_plan_levels": ([_i32, _i32, _i32, _i64p, _i64p], ctypes.c_int),
+    "mtb_align_fused_workspace": ([_i32, _i32, _i32, _i64p, _i64p], ctypes.c_int),
 }
 
 _lock = threading.Lock()

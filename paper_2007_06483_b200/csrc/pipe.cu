@@ -1,0 +1,963 @@
+// The fused alignment pipeline: preprocess (K1 + medians + K3) and the
+// coarse-to-fine search (K4) of a whole batch of exposure pairs, software-
+// pipelined over ONE launch per image so the gray pyramids never leave L2.
+//
+// Reference path (bit-exact): pipeline.py:80-90 -> build_mtb_pyramid
+// (image.py:58-68, pyramid.py:17-62, threshold.py:25-88) -> find_offset
+// (search.py:53-95, kernels/_native.pyx:73-111).
+//
+// Launch j (one 512-thread CTA per SM, programmatic dependent launches):
+//   1. TMA-prefetch this CTA's first RGB tiles of image j      (independent)
+//   2. griddepcontrol.wait: launch j-1 (and so every earlier one) is complete
+//   3. medians of image j-1 from its histograms (every CTA, redundantly)
+//   4. K3: threshold + bit-pack every level of image j-1, reading its gray
+//      from L2 (written by launch j-1 with evict_last) and discarding the
+//      consumed lines so they are never written back
+//   5. K4: one pyramid level for every pair whose maps are ready — pair q
+//      (ref, tgt) is ready at t(q) = max(ref, tgt) + 2 and runs level
+//      n-1-(j-t(q)) in launch j; the warp that completes a (pair, level)
+//      applies the search.py:67 key and publishes the offset for launch j+1
+//   6. K1: gray + pyramid (levels 0..5) + histograms of image j into the gray
+//      slot j % 2 (slot (j-2) % 2 was consumed by launch j-1, which is
+//      complete after step 2)
+// HBM traffic per image is the RGB read plus the packed maps; the gray
+// round trip (32 MB per 24 MP image) stays in L2.
+#include <cstdlib>
+#include <cstring>
+#include <vector>
+
+#include "k1_tile.cuh"
+#include "swar.cuh"
+
+namespace mtb {
+
+constexpr int kPipeMaxLevels = 6;
+constexpr int kPipeMaxItems = 96;
+constexpr int kPipeWarps = kK1Threads / 32;   // 16
+
+struct PipeItem {
+  int pair;      // index into acc/errs/done
+  int ref, tgt;  // image indices
+  int level;
+  int tile0;     // first search warp-tile of this item in this launch
+};
+
+struct PipeArgs {
+  K1Args g;                          // K1 geometry; g.gray = slot base, g.gray_img_stride = slot stride
+  int n;                             // pyramid levels (<= 6)
+  int tol;
+  int nw32[kPipeMaxLevels];          // u32 words per packed row
+  int64_t bit_off32[kPipeMaxLevels]; // u32 word offset of level k in an image's map arena
+  int th_units0[kPipeMaxLevels + 1]; // prefix of threshold units (rows x 32-word chunks) per level
+  int th_cpr[kPipeMaxLevels];        // 32-word chunks per row
+  uint32_t tx_magic;                 // t / tiles_x == umulhi(t, tx_magic) (tiles_x > 1)
+  int th_pad_words;                  // levels 0..3 row-padding words not covered by tiles
+  uint32_t* mtb;                     // map arenas, u32 view; image stride bit_img_words32
+  uint32_t* excl;
+  int64_t bit_img_words32;
+  int32_t* medians;                  // [img][n]
+  int32_t* acc;                      // [P][n][2]
+  unsigned long long* errs;          // [P][n][9]
+  uint32_t* done;                    // [P][n]
+  uint32_t* ctr;                     // [launch][16] aux task stripes, then [launch] K1 tile counters; zeroed
+  int n_launch;
+  int search_first;                  // aux task order (MTB_PIPE_SEARCH_FIRST)
+  int j;                             // this launch's index
+  int k1_img;                        // image of the K1 part, or -1
+  int th_img;                        // image of the K3 part, or -1
+  int n_items;
+  int search_tiles;
+  unsigned long long* trace;         // optional [launch][cta][8] %globaltimer stamps (diagnostics)                  // total search warp-tiles of this launch
+  PipeItem items[kPipeMaxItems];
+};
+
+// Per-level threshold constants (threshold.py:42-56), in shared memory.
+struct ThConst {
+  uint32_t med;     // median replicated in 4 bytes (VABSDIFF4 operand)
+  uint32_t ym;      // (255 - median) replicated: x > median <=> x + ym carries out of the byte
+  uint32_t yml;     // ym & 0x7f7f7f7f
+  int med_lo;       // median <= 127 (ym bit 7 set): carry = (x | s) bit 7, else (x & s) bit 7
+};
+
+// Warp roles: warps 0..7 = two K1 groups streaming image j (never wait on
+// earlier launches: the gray ring has 3 slots), warps 8..15 = the aux warps
+// (K3 + search) which wait for launch j-1.
+constexpr int kPK1Groups = 2;
+constexpr int kPK1Warps = 4 * kPK1Groups;
+constexpr int kPAuxWarps = kPipeWarps - kPK1Warps;
+constexpr int kPStages = 3;
+constexpr int kPGraySlots = 3;
+
+// Per-aux-warp staging of one search warp-tile: 8 output rows x 32 words of
+// the reference maps, 10 source rows x 35 words of the target maps.
+struct SearchStage {
+  uint32_t a[8][32], ea[8][32];
+  uint32_t b[10][36], eb[10][36];
+};
+
+struct PipeSmem {
+  uint32_t hist[6][256];                                  // 1 KB-aligned levels (see k1_tile.cuh)
+  uint8_t rgb[kPK1Groups][kPStages][kK1TileBytes];
+  SearchStage srch[kPAuxWarps];
+  uint8_t l3[kPK1Groups][2][4][32];
+  unsigned long long full[kPK1Groups][kPStages];
+  int tile_of[kPK1Groups][kPStages];                      // tile in each ring stage (-1: no more)
+  ThConst th[kPipeMaxLevels];
+  int last;
+  int next;                                               // aux task queue head
+  unsigned scnt[kPipeMaxItems][9];                        // per-item partial search counts
+};
+constexpr int kPipeSmemBytes = (int)sizeof(PipeSmem) + 1024;
+
+__device__ __forceinline__ void grid_dep_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void grid_dep_launch() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+
+// Lower median of one level's spread histogram (threshold.py:31-39): the
+// smallest m with cumsum[m] >= (total + 1) / 2.  One warp; lane owns 8 bins.
+__device__ __forceinline__ int warp_median(const uint32_t* spread, int lane) {
+  uint32_t bins[8];
+  uint32_t s = 0;
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    bins[i] = __ldcg(spread + (lane * 8 + i) * kHistStrideK1);
+    s += bins[i];
+  }
+  uint32_t incl = s;
+#pragma unroll
+  for (int d = 1; d < 32; d <<= 1) {
+    const uint32_t v = __shfl_up_sync(0xffffffffu, incl, d);
+    if (lane >= d) incl += v;
+  }
+  const uint32_t total = __shfl_sync(0xffffffffu, incl, 31);
+  const uint32_t target = (total + 1) >> 1;
+  const unsigned mask = __ballot_sync(0xffffffffu, incl >= target);
+  if (total == 0) return 0;   // empty level cannot occur (levels are >= 1x1)
+  const int L = __ffs(mask) - 1;
+  int med = 0;
+  if (lane == L) {
+    uint32_t c = incl - s;
+    for (int i = 0; i < 8; ++i) {
+      c += bins[i];
+      if (c >= target) { med = lane * 8 + i; break; }
+    }
+  }
+  return __shfl_sync(0xffffffffu, med, L);
+}
+
+// ---- K3 part ---------------------------------------------------------------
+// Bits of 32 gray pixels (8 words) -> MTB word and exclusion word.
+//   mtb  : g > med               — byte carry-out of g + (255 - med), MAJ(x7, ym7, s7)
+//   excl : |g - med| > tol       — d = VABSDIFF4(g, med); carry-out of d + (255 - tol)
+// With the per-level bit 7 of the addend known, MAJ is one LOP3 that also
+// masks bit 7; the four flags of a word are gathered by one multiply.
+__device__ __forceinline__ void th_word(const uint32_t (&g)[8], const ThConst& c, uint32_t yt, uint32_t ytl,
+                                        int valid, uint32_t& mw, uint32_t& ew) {
+  constexpr uint32_t H = 0x80808080u, L7 = 0x7f7f7f7fu;
+  uint32_t m = 0, e = 0;
+#pragma unroll
+  for (int k = 0; k < 8; ++k) {
+    const uint32_t x = g[k];
+    const uint32_t s = (x & L7) + c.yml;
+    const uint32_t gm = ((x & c.ym) | (x & s) | (c.ym & s)) & H;      // MAJ: byte carry-out of x + (255 - med)
+    uint32_t d;
+    asm("vabsdiff4.u32.u32.u32 %0, %1, %2, %3;" : "=r"(d) : "r"(x), "r"(c.med), "r"(0u));
+    const uint32_t sd = (d & L7) + ytl;
+    const uint32_t ge = ((d & yt) | (d & sd) | (yt & sd)) & H;        // carry-out of |x - med| + (255 - tol)
+    // flags at bits 7,15,23,31 -> bits 28..31 of the product -> bits 4k..4k+3
+    m = (((gm * 0x00204081u) >> (28 - 4 * k)) & (0xfu << (4 * k))) | m;
+    e = (((ge * 0x00204081u) >> (28 - 4 * k)) & (0xfu << (4 * k))) | e;
+  }
+  const uint32_t keep = valid >= 32 ? 0xffffffffu : (valid <= 0 ? 0u : ((1u << valid) - 1u));
+  mw = m & keep;
+  ew = e & keep;
+}
+
+// Unit u of the tile-major threshold sequence: 32 bitmap words of one level.
+// Levels 0..3: words in tile order (tile, row, word) — a unit is 1 KB of
+// contiguous gray; levels 4..5: row-major words (a word spans 2 or 4 tiles).
+struct ThUnit {
+  int k;            // level
+  int64_t out;      // bitmap word index within the image's arena (u32), or -1
+  int valid;        // valid pixels of the word
+  const uint8_t* p; // levels 0..3: the word's 32 gray bytes
+  int y, j;         // levels 4..5: word coordinates
+};
+
+__device__ __forceinline__ ThUnit th_unit(const PipeArgs& a, const uint8_t* slot, int u, int lane) {
+  ThUnit r;
+  int k = 0;
+#pragma unroll
+  for (int i = 1; i < kPipeMaxLevels; ++i)
+    if (i < a.n && u >= a.th_units0[i]) k = i;
+  r.k = k;
+  r.p = nullptr;
+  const int f = (u - a.th_units0[k]) * 32 + lane;   // word index in this level's sequence
+  if (k <= 3) {
+    const int wpr = 8 >> k, lwpr = 3 - k;            // words per tile row
+    const int lwpt = 8 - 2 * k;                      // log2 words per tile
+    const int t = f >> lwpt;
+    const int rem = f & ((1 << lwpt) - 1);
+    const int row = rem >> lwpr, c = rem & (wpr - 1);
+    const int ty = t / a.g.tiles_x, tx = t - ty * a.g.tiles_x;
+    r.y = ty * (kK1TileRows >> k) + row;
+    r.j = tx * wpr + c;
+    r.p = slot + (int64_t)t * kTileGrayBytes + tm_off(k) + row * tm_pitch(k) + c * 32;
+    const bool ok = t < a.g.tiles_x * a.g.tiles_y && r.y < a.g.lh[k] && r.j < a.nw32[k];
+    r.out = ok ? a.bit_off32[k] + (int64_t)r.y * a.nw32[k] + r.j : -1;
+  } else {
+    r.y = f / a.nw32[k];
+    r.j = f - r.y * a.nw32[k];
+    r.out = r.y < a.g.lh[k] ? a.bit_off32[k] + f : -1;
+  }
+  r.valid = a.g.lw[k] - 32 * r.j;
+  return r;
+}
+
+__device__ __forceinline__ int div_tiles_x(const PipeArgs& a, int t) {
+  return a.g.tiles_x == 1 ? t : (int)__umulhi((uint32_t)t, a.tx_magic);
+}
+
+// Levels 0..3: the level's bitmap words in tile order (tile, row, word); a
+// unit is 32 words = 1 KB of contiguous tile-major gray.  NU units per warp
+// iteration keep NU x 1 KB of loads in flight per warp.
+template <int K>
+__device__ __forceinline__ int th_level_units(const PipeArgs& a) {
+  return (int)((((int64_t)a.g.tiles_x * a.g.tiles_y << (8 - 2 * K)) + 31) >> 5);
+}
+
+// One warp iteration: units u0, u0 + nwarps, ... (NU of them).
+// One task of levels 0..3: 4 consecutive units (4 KB of tile-major gray),
+// split in an issue half (addresses + all eight 16-B loads per lane) and a
+// finish half (threshold, store, discard) so a warp can have the next task's
+// loads in flight while it computes the current one.
+constexpr int kK3NU = 4;
+struct K3Task {
+  uint4 v[kK3NU][2];
+  uint32_t goff[kK3NU];  // byte offset of the lane's 32 gray bytes in the slot
+  int out[kK3NU];        // bitmap word (u32) in the image's arena, or -1
+  int valid[kK3NU];      // valid pixels of the word
+  int K;                 // level
+  uint32_t in;           // bit i: unit i exists (load was real)
+};
+
+__device__ __forceinline__ void k3_issue(const PipeArgs& a, const uint8_t* slot, int K, int u0, int lane, K3Task& T) {
+  const int lwpr = 3 - K, wpr = 1 << lwpr;   // words per tile row
+  const int lwpt = 8 - 2 * K;                // log2 words per tile
+  const int rows = kK1TileRows >> K;
+  const int ntiles = a.g.tiles_x * a.g.tiles_y;
+  const int units = (int)((((int64_t)ntiles << lwpt) + 31) >> 5);
+  const int nw = a.nw32[K], lh = a.g.lh[K], lw = a.g.lw[K];
+  const int boff = (int)a.bit_off32[K];
+  const int toff = tm_off(K), tpitch = tm_pitch(K);
+  T.K = K;
+  T.in = 0;
+#pragma unroll
+  for (int i = 0; i < kK3NU; ++i) {
+    const int u = u0 + i;
+    const int f = (u < units ? u : u0) * 32 + lane;
+    const int t = f >> lwpt;
+    const int rem = f & ((1 << lwpt) - 1);
+    const int row = rem >> lwpr, cc = rem & (wpr - 1);
+    const int ty = div_tiles_x(a, t), tx = t - ty * a.g.tiles_x;
+    const int y = ty * rows + row, j = tx * wpr + cc;
+    // lanes past the last tile (levels 2-3 pack several tiles per unit) read
+    // tile 0 and neither store nor discard
+    const bool in = u < units && t < ntiles;
+    T.in |= (uint32_t)in << i;
+    T.goff[i] = (uint32_t)(in ? t : 0) * kTileGrayBytes + toff + row * tpitch + cc * 32;
+    T.out[i] = (in && y < lh && j < nw) ? boff + y * nw + j : -1;
+    T.valid[i] = lw - 32 * j;
+    const uint4* q = reinterpret_cast<const uint4*>(slot + T.goff[i]);
+    T.v[i][0] = __ldcs(q);
+    T.v[i][1] = __ldcs(q + 1);
+  }
+}
+
+__device__ __forceinline__ void k3_finish(const uint8_t* slot, uint32_t* mtb, uint32_t* excl, const ThConst* th,
+                                          uint32_t yt, uint32_t ytl, const K3Task& T, int lane) {
+  const ThConst c = th[T.K];
+#pragma unroll
+  for (int i = 0; i < kK3NU; ++i) {
+    const uint32_t g[8] = {T.v[i][0].x, T.v[i][0].y, T.v[i][0].z, T.v[i][0].w,
+                           T.v[i][1].x, T.v[i][1].y, T.v[i][1].z, T.v[i][1].w};
+    uint32_t m, e;
+    th_word(g, c, yt, ytl, T.valid[i], m, e);
+    if (T.out[i] >= 0) {
+      mtb[T.out[i]] = m;
+      excl[T.out[i]] = e;
+    }
+  }
+  __syncwarp();
+  // 4 consecutive lanes read one 128-B gray line: drop it from L2 without write-back.
+  if ((lane & 3) == 0) {
+#pragma unroll
+    for (int i = 0; i < kK3NU; ++i)
+      if ((T.in >> i) & 1u) asm volatile("discard.global.L2 [%0], 128;" ::"l"(slot + T.goff[i]) : "memory");
+  }
+}
+
+// 32 gray bytes of a level-4/5 word gathered from the tiles it spans
+// (K = 4: two 16-px tile rows, K = 5: four 8-px tile rows).
+template <int K>
+__device__ __forceinline__ void th_gather45(const PipeArgs& a, const uint8_t* slot, const ThUnit& r, uint32_t (&g)[8]) {
+  constexpr int tw = kK1TilePx >> K;
+  constexpr int rows = kK1TileRows >> K;
+  constexpr int nq = 32 / tw;
+  const int ty = r.y / rows, row = r.y - ty * rows;
+#pragma unroll
+  for (int q = 0; q < nq; ++q) {
+    const int tx = nq * r.j + q;
+    uint32_t w4[4] = {0, 0, 0, 0};
+    if (tx < a.g.tiles_x) {
+      const uint8_t* p = slot + (int64_t)(ty * a.g.tiles_x + tx) * kTileGrayBytes + tm_off(K) + row * tm_pitch(K);
+      if (tw == 16) {
+        const uint4 v = *reinterpret_cast<const uint4*>(p);
+        w4[0] = v.x; w4[1] = v.y; w4[2] = v.z; w4[3] = v.w;
+      } else {
+        const uint2 v = *reinterpret_cast<const uint2*>(p);
+        w4[0] = v.x; w4[1] = v.y;
+      }
+    }
+#pragma unroll
+    for (int i = 0; i < tw / 4; ++i) g[q * (tw / 4) + i] = w4[i];
+  }
+}
+
+// ---- K4 part ---------------------------------------------------------------
+__device__ __forceinline__ void cp_async4(uint32_t* dst, const uint32_t* src, bool ok) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;" ::"r"(smem_addr(dst)), "l"(src), "r"(ok ? 4 : 0)
+               : "memory");
+}
+
+// One search warp-tile (8 output rows x 32 words) of item `it`, staged into
+// this warp's shared buffer with cp.async (every load in flight at once),
+// then: per output word 9 x (LOP3 + LOP3 + POPC) over a 3-row register window
+// of the target rows pre-shifted by bx-1, bx, bx+1 (funnel shifts).
+__device__ __forceinline__ void pipe_search_tile(const PipeArgs& a, const PipeItem& it, int tile, int lane,
+                                                 SearchStage& sm, unsigned* scnt) {
+  const int k = it.level;
+  const int h = a.g.lh[k];
+  const int nw = a.nw32[k];
+  const int cpr = (nw + 31) >> 5;
+  const int rb = tile / cpr, cb = tile - rb * cpr;
+  const int y0 = rb * 8;
+  const int j0 = cb * 32;
+  const int n = a.n;
+  int bx = 0, by = 0;
+  if (k + 1 < n) {
+    const int32_t* prev = a.acc + ((int64_t)it.pair * n + (k + 1)) * 2;
+    bx = 2 * __ldcg(prev);
+    by = 2 * __ldcg(prev + 1);
+  }
+  const uint32_t* A = a.mtb + (int64_t)it.ref * a.bit_img_words32 + a.bit_off32[k];
+  const uint32_t* EA = a.excl + (int64_t)it.ref * a.bit_img_words32 + a.bit_off32[k];
+  const uint32_t* B = a.mtb + (int64_t)it.tgt * a.bit_img_words32 + a.bit_off32[k];
+  const uint32_t* EB = a.excl + (int64_t)it.tgt * a.bit_img_words32 + a.bit_off32[k];
+  const int qb = bx >> 5;
+  // ---- stage: A/EA rows y0..y0+7, words j0..j0+31; B/EB source rows
+  //      y0-by-1 .. y0-by+8, words j0-qb-2 .. j0-qb+32
+  {
+    const int j = j0 + lane;
+#pragma unroll
+    for (int r = 0; r < 8; ++r) {
+      const int y = y0 + r;
+      const bool ok = y < h && j < nw;
+      const int64_t o = ok ? (int64_t)y * nw + j : 0;
+      cp_async4(&sm.a[r][lane], A + o, ok);
+      cp_async4(&sm.ea[r][lane], EA + o, ok);
+    }
+    const int sy0 = y0 - by - 1;
+#pragma unroll
+    for (int r = 0; r < 10; ++r) {
+      const int sy = sy0 + r;
+      const bool rok = sy >= 0 && sy < h;
+#pragma unroll
+      for (int c = 0; c < 2; ++c) {
+        const int col = lane + 32 * c;
+        if (c == 0 || col < 35) {
+          const int idx = j0 - qb - 2 + col;
+          const bool ok = rok && idx >= 0 && idx < nw;
+          const int64_t o = ok ? (int64_t)sy * nw + idx : 0;
+          cp_async4(&sm.b[r][col], B + o, ok);
+          cp_async4(&sm.eb[r][col], EB + o, ok);
+        }
+      }
+    }
+    asm volatile("cp.async.wait_all;" ::: "memory");
+    __syncwarp();
+  }
+  int o[3], r[3];
+#pragma unroll
+  for (int d = 0; d < 3; ++d) {
+    const int dx = bx + d - 1;
+    o[d] = (dx >> 5) - qb;   // in {-1, 0, 1}
+    r[d] = dx & 31;
+  }
+  // staged source row lr shifted by bx-1, bx, bx+1: W[j-q] = w[2-o], W[j-q-1] = w[1-o], w[i] = staged word lane+i
+  auto shifted = [&](int lr, uint32_t (&sb)[3], uint32_t (&se)[3]) {
+    uint32_t wb[4], we[4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      wb[i] = sm.b[lr][lane + i];
+      we[i] = sm.eb[lr][lane + i];
+    }
+#pragma unroll
+    for (int d = 0; d < 3; ++d) {
+      const uint32_t hb = o[d] < 0 ? wb[3] : (o[d] == 0 ? wb[2] : wb[1]);
+      const uint32_t lb = o[d] < 0 ? wb[2] : (o[d] == 0 ? wb[1] : wb[0]);
+      const uint32_t he = o[d] < 0 ? we[3] : (o[d] == 0 ? we[2] : we[1]);
+      const uint32_t le = o[d] < 0 ? we[2] : (o[d] == 0 ? we[1] : we[0]);
+      sb[d] = shifted_word(lb, hb, r[d]);
+      se[d] = shifted_word(le, he, r[d]);
+    }
+  };
+  unsigned cnt[9];
+#pragma unroll
+  for (int i = 0; i < 9; ++i) cnt[i] = 0;
+  // output row y0+rr needs staged source rows rr+2 (ddy=-1), rr+1 (0), rr (+1)
+  uint32_t b0[3], e0[3], b1[3], e1[3];
+  shifted(0, b0, e0);
+  shifted(1, b1, e1);
+#pragma unroll
+  for (int rr = 0; rr < 8; ++rr) {
+    uint32_t b2[3], e2[3];
+    shifted(rr + 2, b2, e2);
+    const uint32_t av = sm.a[rr][lane], ev = sm.ea[rr][lane];
+#pragma unroll
+    for (int d = 0; d < 3; ++d) {
+      cnt[0 + d] += __popc((av ^ b2[d]) & ev & e2[d]);
+      cnt[3 + d] += __popc((av ^ b1[d]) & ev & e1[d]);
+      cnt[6 + d] += __popc((av ^ b0[d]) & ev & e0[d]);
+    }
+#pragma unroll
+    for (int d = 0; d < 3; ++d) {
+      b0[d] = b1[d]; e0[d] = e1[d];
+      b1[d] = b2[d]; e1[d] = e2[d];
+    }
+  }
+  __syncwarp();   // the staging buffer is reused by the next tile
+  // CTA-level partial counts (shared atomics); flushed once per CTA and item
+  // by pipe_search_flush after all of the CTA's tasks are done.
+#pragma unroll
+  for (int i = 0; i < 9; ++i) {
+    const unsigned v = warp_sum(cnt[i]);
+    if (lane == 0 && v) atomicAdd(scnt + i, v);
+  }
+}
+
+// After the CTA's last task: add its partial counts of item `it` to the
+// pair's 9 u64 counters; the last CTA to do so applies the search.py:67 key
+// (err, |ddx|+|ddy|, index) and publishes the level's offset.
+__device__ __forceinline__ void pipe_search_flush(const PipeArgs& a, const PipeItem& it, const unsigned* scnt) {
+  const int n = a.n, k = it.level;
+  unsigned long long* errs = a.errs + ((int64_t)it.pair * n + k) * 9;
+  for (int i = 0; i < 9; ++i)
+    if (scnt[i]) atomicAdd(errs + i, (unsigned long long)scnt[i]);
+  __threadfence();
+  uint32_t* done = a.done + (int64_t)it.pair * n + k;
+  if (atomicAdd(done, 1u) == gridDim.x - 1) {
+    __threadfence();
+    int bx = 0, by = 0;
+    if (k + 1 < n) {
+      const int32_t* prev = a.acc + ((int64_t)it.pair * n + (k + 1)) * 2;
+      bx = 2 * __ldcg(prev);
+      by = 2 * __ldcg(prev + 1);
+    }
+    int best = 0, bd = 0;
+    unsigned long long be = 0;
+    for (int i = 0; i < 9; ++i) {
+      const unsigned long long e = __ldcg(errs + i);
+      const int d = abs(i % 3 - 1) + abs(i / 3 - 1);
+      if (i == 0 || e < be || (e == be && d < bd)) { best = i; be = e; bd = d; }
+    }
+    int32_t* out = a.acc + ((int64_t)it.pair * n + k) * 2;
+    out[0] = bx + best % 3 - 1;
+    out[1] = by + best / 3 - 1;
+  }
+}
+
+// ---- the non-K1 work of a launch as a per-CTA task queue -------------------
+// Phases: K3 levels 0..3 (tile order, NU consecutive units per task), levels
+// 4..5, uncovered row padding, search warp-tiles.  CTA c owns the slice
+// [c*T/G, (c+1)*T/G) of every phase's T tasks; its warps pull tasks from a
+// shared-memory counter — the aux warps right after the grid dependency
+// wait, the K1 warps once their tiles are done — so the CTA's K1 and aux
+// work finish together.
+constexpr int kAuxPhases = 7;
+static_assert(4 * sizeof(SearchStage) <= kK1TileBytes, "K1 warps stage search tiles in a ring stage");
+
+struct AuxCtx {
+  const uint8_t* slot;
+  uint32_t* mtb;
+  uint32_t* excl;
+  uint32_t yt, ytl;
+  int lane;
+  SearchStage* stage;
+  bool tracer;   // diagnostics: this warp stamps phase starts (MTB_PIPE_TRACE)
+};
+
+__device__ __forceinline__ void named_bar(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory"); }
+
+// Global task count of phase p.
+__device__ __forceinline__ int aux_phase_tasks(const PipeArgs& a, int p) {
+  const bool th = a.th_img >= 0;
+  switch (p) {
+    case 0: return th ? (th_level_units<0>(a) + 3) / 4 : 0;
+    case 1: return th && a.n > 1 ? (th_level_units<1>(a) + 3) / 4 : 0;
+    case 2: return th && a.n > 2 ? (th_level_units<2>(a) + 3) / 4 : 0;
+    case 3: return th && a.n > 3 ? (th_level_units<3>(a) + 3) / 4 : 0;
+    case 4: return th ? a.th_units0[a.n] - a.th_units0[a.n < 4 ? a.n : 4] : 0;
+    case 5: return th ? (a.th_pad_words + 31) / 32 : 0;
+    default: return a.search_tiles;   // 6
+  }
+}
+
+// Zero padding words: flat index f over levels 0..3 of (row, uncovered word).
+__device__ __forceinline__ void aux_pad(const PipeArgs& a, const AuxCtx& x, int f) {
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    if (k >= a.n) return;
+    const int j0 = a.g.tiles_x * (8 >> k);
+    const int npad = a.nw32[k] - j0;
+    if (npad <= 0) continue;
+    const int cnt = npad * a.g.lh[k];
+    if (f < cnt) {
+      const int y = f / npad, j = j0 + (f - y * npad);
+      const int64_t o = a.bit_off32[k] + (int64_t)y * a.nw32[k] + j;
+      x.mtb[o] = 0u;
+      x.excl[o] = 0u;
+      return;
+    }
+    f -= cnt;
+  }
+}
+
+// Runs global task `t` of phase `p`.
+__device__ __forceinline__ void aux_run(const PipeArgs& a, PipeSmem& S, const AuxCtx& x, int p, int t) {
+  switch (p) {
+    case 4: {
+      const ThUnit r = th_unit(a, x.slot, a.th_units0[a.n < 4 ? a.n : 4] + t, x.lane);
+      uint32_t g8[8];
+      if (r.k == 4) th_gather45<4>(a, x.slot, r, g8);
+      else th_gather45<5>(a, x.slot, r, g8);
+      uint32_t m, e;
+      th_word(g8, S.th[r.k], x.yt, x.ytl, r.valid, m, e);
+      if (r.out >= 0) { x.mtb[r.out] = m; x.excl[r.out] = e; }
+      break;
+    }
+    case 5: {
+      const int f = t * 32 + x.lane;
+      if (f < a.th_pad_words) aux_pad(a, x, f);
+      break;
+    }
+    default: {
+      int it = 0;
+      while (it + 1 < a.n_items && t >= a.items[it + 1].tile0) ++it;
+      pipe_search_tile(a, a.items[it], t - a.items[it].tile0, x.lane, *x.stage, S.scnt[it]);
+      break;
+    }
+  }
+}
+
+// The CTA's share of every phase's tasks, pulled by its warps from a
+// shared-memory counter: the aux warps right after the grid dependency wait,
+// the K1 warps once the image's tiles are exhausted (tiles are claimed
+// dynamically, so every CTA's K1 warps run dry at about the same time and the
+// equal static slices stay balanced).  Task order within the CTA: K3 levels
+// 0..3 (4 units each), levels 4..5, padding, search tiles — or search first
+// (a.search_first).
+__device__ __forceinline__ int aux_phase_of(const PipeArgs& a, int q) {
+  return a.search_first ? (q == 0 ? 6 : q - 1) : q;
+}
+
+__device__ __noinline__ void aux_drain(const PipeArgs& a, PipeSmem& S, const AuxCtx& x) {
+  const int G = gridDim.x, c = blockIdx.x;
+  int lo[kAuxPhases], cnt[kAuxPhases];
+#pragma unroll
+  for (int q = 0; q < kAuxPhases; ++q) {
+    const int T = aux_phase_tasks(a, aux_phase_of(a, q));
+    lo[q] = (int)((int64_t)c * T / G);
+    cnt[q] = (int)((int64_t)(c + 1) * T / G) - lo[q];
+  }
+  for (;;) {
+    int t = 0;
+    if (x.lane == 0) t = atomicAdd(&S.next, 1);
+    t = __shfl_sync(0xffffffffu, t, 0);
+    int q = 0;
+    while (q < kAuxPhases && t >= cnt[q]) t -= cnt[q++];
+    if (q == kAuxPhases) return;
+    const int p = aux_phase_of(a, q);
+    if (x.tracer && x.lane == 0 && a.trace) {
+      unsigned long long* slot = a.trace + ((int64_t)a.j * gridDim.x + blockIdx.x) * 16 + 8 + p;
+      if (*slot == 0) {
+        unsigned long long tt;
+        asm volatile("mov.u64 %0, %globaltimer;" : "=l"(tt));
+        *slot = tt;
+      }
+    }
+    if (p < 4) {
+      K3Task T;
+      k3_issue(a, x.slot, p, 4 * (lo[q] + t), x.lane, T);
+      k3_finish(x.slot, x.mtb, x.excl, S.th, x.yt, x.ytl, T, x.lane);
+    } else {
+      aux_run(a, S, x, p, lo[q] + t);
+    }
+  }
+}
+
+__global__ void __launch_bounds__(kK1Threads, 1) pipe_kernel(const __grid_constant__ PipeArgs a,
+                                                             const __grid_constant__ CUtensorMap rgb_map) {
+  extern __shared__ __align__(128) uint8_t pipe_smem_raw[];
+  const uint32_t raw = smem_addr(pipe_smem_raw);
+  PipeSmem& S = *reinterpret_cast<PipeSmem*>(pipe_smem_raw + ((1024u - (raw & 1023u)) & 1023u));
+  const int tid = threadIdx.x;
+  const int lane = tid & 31;
+  const int warp = tid >> 5;
+  auto stamp = [&](int i) {
+    if (a.trace && (tid & 255) == 0) {
+      unsigned long long t;
+      asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+      a.trace[((int64_t)a.j * gridDim.x + blockIdx.x) * 16 + i] = t;
+    }
+  };
+
+  if (warp < kPK1Warps) {
+    // ======================= K1 warps: image k1_img ==========================
+    const int g = warp >> 2;          // K1 group
+    const int t = tid & 127;
+    const int wg = warp & 3;
+    const int kt = tid;               // 0..255 among the K1 threads
+    const uint32_t hb = smem_addr(&S.hist[0][0]);
+    stamp(0);
+    if (a.k1_img >= 0) {
+      const int tiles_img = a.g.tiles_x * a.g.tiles_y;
+      uint32_t* ctr = a.ctr + a.j;   // K1 tile counter of this launch
+      uint64_t pol_first;
+      asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol_first));
+      for (int i = kt; i < 6 * 256; i += 32 * kPK1Warps) (&S.hist[0][0])[i] = 0;
+      // Claim the next tile of the image for ring stage `stage` (launch-wide
+      // counter: CTAs that start late take fewer tiles) and start its copy;
+      // past the end, complete the stage's phase with tile -1.
+      auto claim = [&](int stage) {
+        int tile = (int)atomicAdd(ctr, 1u);
+        if (tile >= tiles_img) tile = -1;
+        S.tile_of[g][stage] = tile;
+        if (tile >= 0) {
+          const int ty = div_tiles_x(a, tile), tx = tile - ty * a.g.tiles_x;
+          mbar_expect_tx(&S.full[g][stage], kK1TileBytes);
+          tma_tile(S.rgb[g][stage], &rgb_map, (kK1RowBytes / 4) * tx, kK1TileRows * ty, a.k1_img, &S.full[g][stage],
+                   pol_first);
+        } else {
+          asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_addr(&S.full[g][stage])) : "memory");
+        }
+      };
+      if (t == 0) {
+        for (int s = 0; s < kPStages; ++s) mbar_init(&S.full[g][s], 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        for (int s = 0; s < kPStages; ++s) claim(s);
+      }
+      named_bar(5, 32 * kPK1Warps);   // hist zeroed, mbarriers initialised
+      uint8_t* slot = a.g.gray + (int64_t)(a.k1_img % kPGraySlots) * a.g.gray_img_stride;
+      int k = 0, ptx = 0, pty = 0, ptile = 0;
+      bool pfull = true;
+      for (;; ++k) {
+        const int stage = k % kPStages;
+        mbar_wait(&S.full[g][stage], (uint32_t)(k / kPStages) & 1u);
+        const int tile = *reinterpret_cast<volatile int*>(&S.tile_of[g][stage]);
+        if (tile < 0) break;
+        const int ty = div_tiles_x(a, tile), tx = tile - ty * a.g.tiles_x;
+        const bool full = (ty * kK1TileRows + kK1TileRows <= a.g.h) && (tx * kK1TilePx + kK1TilePx <= a.g.w);
+        uint2 v[8][3];
+        {
+          const uint8_t* src = S.rgb[g][stage] + (8 * wg) * kK1RowBytes + 24 * lane;
+#pragma unroll
+          for (int r = 0; r < 8; ++r)
+#pragma unroll
+            for (int c = 0; c < 3; ++c) v[r][c] = *reinterpret_cast<const uint2*>(src + r * kK1RowBytes + 8 * c);
+        }
+        group_bar(g);
+        if (t == 0) {
+          asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+          claim(stage);
+        }
+        if (k > 0 && a.g.nl >= 5 && wg == ((k - 1) & 3))
+          k1_levels45_tm(a.g, slot + (int64_t)ptile * kTileGrayBytes, S.l3[g][(k - 1) & 1], ptx, pty, lane, hb,
+                         pfull);
+        uint8_t* tg = slot + (int64_t)tile * kTileGrayBytes;
+        uint8_t* l3_slot = &S.l3[g][k & 1][wg][lane];
+        if (full)
+          k1_block_tm<true>(a.g, tg, v, tx, ty, wg, lane, hb, l3_slot);
+        else
+          k1_block_tm<false>(a.g, tg, v, tx, ty, wg, lane, hb, l3_slot);
+        ptx = tx;
+        pty = ty;
+        ptile = tile;
+        pfull = full;
+      }
+      group_bar(g);
+      if (k > 0 && a.g.nl >= 5 && wg == ((k - 1) & 3))
+        k1_levels45_tm(a.g, slot + (int64_t)ptile * kTileGrayBytes, S.l3[g][(k - 1) & 1], ptx, pty, lane, hb,
+                       pfull);
+      named_bar(5, 32 * kPK1Warps);
+      stamp(1);
+      uint32_t* gh = a.g.hist + (int64_t)a.k1_img * a.g.hist_img_stride;
+      for (int i = kt; i < a.g.nl * 256; i += 32 * kPK1Warps) {
+        const uint32_t c = (&S.hist[0][0])[i];
+        if (c) atomicAdd(&gh[(int64_t)i * kHistStrideK1], c);
+      }
+      // The last CTA to finish image k1_img publishes its medians
+      // (threshold.py:31-39).  Counter: word 1 of bin 0's 128-B line.
+      named_bar(5, 32 * kPK1Warps);
+      if (kt == 0) {
+        __threadfence();
+        S.last = atomicAdd(gh + 1, 1u) == gridDim.x - 1;
+      }
+      named_bar(5, 32 * kPK1Warps);
+      if (S.last) {
+        __threadfence();
+        if (warp < a.n) {
+          const int m = warp_median(gh + warp * 256 * kHistStrideK1, lane);
+          if (lane == 0) a.medians[a.k1_img * a.n + warp] = m;
+        }
+      }
+      stamp(2);
+    }
+    // Join the aux work.  The wait also orders the trigger: launch j+1's K1
+    // overwrites the gray slot of image j-2, which launch j-1 reads.
+    grid_dep_wait();
+    grid_dep_launch();
+    asm volatile("bar.sync 9, %0;" ::"r"(kK1Threads) : "memory");   // S.th / S.next ready
+    AuxCtx ax;
+    ax.slot = a.g.gray + (int64_t)((a.th_img >= 0 ? a.th_img : 0) % kPGraySlots) * a.g.gray_img_stride;
+    ax.mtb = a.mtb + (int64_t)(a.th_img >= 0 ? a.th_img : 0) * a.bit_img_words32;
+    ax.excl = a.excl + (int64_t)(a.th_img >= 0 ? a.th_img : 0) * a.bit_img_words32;
+    ax.yt = (uint32_t)(255 - a.tol) * 0x01010101u;
+    ax.ytl = ax.yt & 0x7f7f7f7fu;
+    ax.lane = lane;
+    // search staging in this group's first ring stage (all its TMA copies have landed)
+    ax.stage = reinterpret_cast<SearchStage*>(&S.rgb[warp >> 2][0][0]) + (warp & 3);
+    ax.tracer = true;
+    aux_drain(a, S, ax);
+    stamp(3);
+    named_bar(10, kK1Threads);   // every task of this CTA done
+    return;
+  }
+
+  // ========================= aux warps: K3 + search ==========================
+  const int aw = warp - kPK1Warps;
+  const int at = tid - 32 * kPK1Warps;    // 0..255
+  grid_dep_wait();                         // launch j-1 (and so all earlier) complete
+  grid_dep_launch();
+  stamp(4);
+  if (a.trace && at == 0) {
+    unsigned smid;
+    asm volatile("mov.u32 %0, %smid;" : "=r"(smid));
+    a.trace[((int64_t)a.j * gridDim.x + blockIdx.x) * 16 + 6] = smid;
+  }
+  if (a.th_img >= 0 && at < a.n) {
+    const int med = __ldcg(a.medians + a.th_img * a.n + at);
+    ThConst c;
+    c.med = (uint32_t)med * 0x01010101u;
+    c.ym = (uint32_t)(255 - med) * 0x01010101u;
+    c.yml = c.ym & 0x7f7f7f7fu;
+    c.med_lo = med <= 127;
+    S.th[at] = c;
+  }
+  if (at == 0) S.next = 0;
+  for (int i = at; i < a.n_items * 9; i += 32 * kPAuxWarps) (&S.scnt[0][0])[i] = 0;
+  named_bar(6, 32 * kPAuxWarps);
+  asm volatile("bar.arrive 9, %0;" ::"r"(kK1Threads) : "memory");
+  AuxCtx ax;
+  ax.slot = a.g.gray + (int64_t)((a.th_img >= 0 ? a.th_img : 0) % kPGraySlots) * a.g.gray_img_stride;
+  ax.mtb = a.mtb + (int64_t)(a.th_img >= 0 ? a.th_img : 0) * a.bit_img_words32;
+  ax.excl = a.excl + (int64_t)(a.th_img >= 0 ? a.th_img : 0) * a.bit_img_words32;
+  ax.yt = (uint32_t)(255 - a.tol) * 0x01010101u;
+  ax.ytl = ax.yt & 0x7f7f7f7fu;
+  ax.lane = lane;
+  ax.stage = &S.srch[aw];
+  ax.tracer = true;
+  aux_drain(a, S, ax);
+  stamp(5);
+  named_bar(10, kK1Threads);
+  if (at < a.n_items) pipe_search_flush(a, a.items[at], S.scnt[at]);
+}
+
+bool k1_rgb_supported(int w, int64_t rgb_pitch, int64_t rgb_img_stride, const void* rgb);
+PFN_cuTensorMapEncodeTiled_v12000 k1_encode_tiled();
+int64_t spread_hist_elems(int n_levels);
+
+}  // namespace mtb
+
+using namespace mtb;
+
+extern "C" int mtb_align_fused_workspace(int w, int h, int levels, int64_t* gray_bytes, int64_t* hist_elems) {
+  Plan p;
+  if (!make_plan(w, h, levels, &p)) return -1;
+  const int64_t tiles = (int64_t)((w + kK1TilePx - 1) / kK1TilePx) * ((h + kK1TileRows - 1) / kK1TileRows);
+  if (gray_bytes) *gray_bytes = kPGraySlots * tiles * kTileGrayBytes;
+  if (hist_elems) *hist_elems = spread_hist_elems(p.n);
+  return p.n <= kPipeMaxLevels ? p.n : -1;
+}
+
+extern "C" int mtb_align_fused(const uint8_t* rgb, int64_t rgb_pitch, int64_t rgb_img_stride, int w, int h,
+                               int n_img, int levels, int tol, const int32_t* pairs_host, int n_pairs,
+                               uint8_t* gray_ws, uint32_t* hist_ws, int32_t* medians, uint64_t* mtb,
+                               uint64_t* exclusion, int32_t* acc, unsigned long long* errs, uint32_t* done,
+                               uint32_t* sync_ws, void* stream) {
+  clear_error();
+  MTB_REQUIRE(rgb && gray_ws && hist_ws && medians && mtb && exclusion && sync_ws, "null pointer");
+  MTB_REQUIRE(n_pairs == 0 || (pairs_host && acc && errs && done), "null pair buffers");
+  MTB_REQUIRE(n_img >= 1 && n_img <= 65535, "image count out of range");
+  MTB_REQUIRE(n_pairs >= 0 && n_pairs <= 65535, "pair count out of range");
+  MTB_REQUIRE(tol >= 0 && tol <= 255, "noise tolerance must be in 0..255");
+  MTB_REQUIRE(rgb_pitch >= 3 * (int64_t)w, "rgb pitch smaller than row");
+  Plan p;
+  MTB_REQUIRE(make_plan(w, h, levels, &p), "image must be at least 16x16 and levels >= 1");
+  MTB_REQUIRE(p.n <= kPipeMaxLevels, "fused path supports at most 6 pyramid levels");
+  MTB_REQUIRE(k1_rgb_supported(w, rgb_pitch, rgb_img_stride, rgb),
+              "fused path needs 16-byte aligned RGB rows with 3*W % 4 == 0");
+  const int64_t slot_bytes =
+      (int64_t)((w + kK1TilePx - 1) / kK1TilePx) * ((h + kK1TileRows - 1) / kK1TileRows) * kTileGrayBytes;
+  MTB_REQUIRE(slot_bytes < ((int64_t)1 << 31), "image too large for the fused path");
+  for (int q = 0; q < n_pairs; ++q) {
+    MTB_REQUIRE(pairs_host[2 * q] >= 0 && pairs_host[2 * q] < n_img && pairs_host[2 * q + 1] >= 0 &&
+                    pairs_host[2 * q + 1] < n_img,
+                "pair image index out of range");
+  }
+  cudaStream_t st = as_stream(stream);
+
+  PipeArgs a;
+  std::memset(&a, 0, sizeof(a));
+  K1Args& g = a.g;
+  g.w = w;
+  g.h = h;
+  g.nl = p.n;
+  for (int k = 0; k < 6; ++k) {
+    const int l = k < p.n ? k : p.n - 1;
+    g.off[k] = (int)p.lv[l].gray_off;
+    g.pitch[k] = (int)p.lv[l].gray_pitch;
+    g.lw[k] = k < p.n ? p.lv[k].w : 0;
+    g.lh[k] = k < p.n ? p.lv[k].h : 0;
+  }
+  g.gray = gray_ws;
+  g.gray_img_stride = slot_bytes;   // tile-major slot (k1_tile.cuh kTmOff)
+  g.hist = hist_ws;
+  g.hist_img_stride = spread_hist_elems(p.n);
+  g.tiles_x = (w + kK1TilePx - 1) / kK1TilePx;
+  g.tiles_y = (h + kK1TileRows - 1) / kK1TileRows;
+  g.n_img = 1;
+  g.keep_gray = 1;
+  a.n = p.n;
+  a.tol = tol;
+  a.th_units0[0] = 0;
+  const int ntiles = ((w + kK1TilePx - 1) / kK1TilePx) * ((h + kK1TileRows - 1) / kK1TileRows);
+  a.tx_magic = g.tiles_x > 1 ? (uint32_t)((((uint64_t)1 << 32) + g.tiles_x - 1) / g.tiles_x) : 0u;
+  MTB_REQUIRE(g.tiles_x < 4096, "image too wide for the fused path");
+  for (int k = 0; k < p.n; ++k) {
+    a.nw32[k] = (int)(2 * p.lv[k].nw64);
+    a.bit_off32[k] = 2 * p.lv[k].bit_off;
+    a.th_cpr[k] = (a.nw32[k] + 31) / 32;
+    // levels 0..3: tile-order words (256 >> 2k per tile); 4..5: row-major words
+    const int64_t words = k <= 3 ? (int64_t)ntiles * (256 >> (2 * k)) : (int64_t)a.nw32[k] * p.lv[k].h;
+    a.th_units0[k + 1] = a.th_units0[k] + (int)((words + 31) / 32);
+  }
+  for (int k = p.n + 1; k <= kPipeMaxLevels; ++k) a.th_units0[k] = a.th_units0[p.n];
+  a.th_pad_words = 0;
+  for (int k = 0; k < p.n && k < 4; ++k) {
+    const int npad = a.nw32[k] - g.tiles_x * (8 >> k);
+    if (npad > 0) a.th_pad_words += npad * p.lv[k].h;
+  }
+  a.mtb = reinterpret_cast<uint32_t*>(mtb);
+  a.excl = reinterpret_cast<uint32_t*>(exclusion);
+  a.bit_img_words32 = 2 * p.bit_img_words;
+  a.medians = medians;
+  {
+    const char* sf = getenv("MTB_PIPE_SEARCH_FIRST");
+    a.search_first = sf ? atoi(sf) : 0;
+    const char* tr = getenv("MTB_PIPE_TRACE");   // device address of a [J][grid][8] u64 buffer
+    a.trace = tr ? reinterpret_cast<unsigned long long*>(strtoull(tr, nullptr, 0)) : nullptr;
+  }
+  a.ctr = sync_ws;
+  a.acc = acc;
+  a.errs = errs;
+  a.done = done;
+
+  MTB_CUDA(cudaMemsetAsync(hist_ws, 0, sizeof(uint32_t) * spread_hist_elems(p.n) * n_img, st));
+  if (n_pairs > 0) {
+    MTB_CUDA(cudaMemsetAsync(errs, 0, sizeof(unsigned long long) * 9 * p.n * n_pairs, st));
+    MTB_CUDA(cudaMemsetAsync(done, 0, sizeof(uint32_t) * p.n * n_pairs, st));
+  }
+
+  // Pair q runs level n-1-(j-t(q)) in launch j, t(q) = max(ref, tgt) + 2.
+  std::vector<int> ready(n_pairs);
+  int J = n_img + 1;
+  for (int q = 0; q < n_pairs; ++q) {
+    const int r = pairs_host[2 * q], tg = pairs_host[2 * q + 1];
+    ready[q] = (r > tg ? r : tg) + 2;
+    if (ready[q] + p.n > J) J = ready[q] + p.n;
+  }
+  // sync_ws: 17 counters per launch (mtb_align_fused_workspace: 17 * (n_img + 8) words)
+  MTB_REQUIRE(J <= n_img + 8, "internal: launch count");
+  MTB_CUDA(cudaMemsetAsync(sync_ws, 0, sizeof(uint32_t) * 17 * J, st));
+  a.n_launch = J;
+  int search_tiles_level[kPipeMaxLevels];
+  for (int k = 0; k < p.n; ++k) search_tiles_level[k] = ((p.lv[k].h + 7) / 8) * ((a.nw32[k] + 31) / 32);
+
+  CUtensorMap map;
+  {
+    const cuuint64_t dims[3] = {(cuuint64_t)(3 * (int64_t)w / 4), (cuuint64_t)h, (cuuint64_t)n_img};
+    const cuuint64_t strides[2] = {(cuuint64_t)rgb_pitch, (cuuint64_t)rgb_img_stride};
+    const cuuint32_t box[3] = {kK1RowBytes / 4, kK1TileRows, 1};
+    const cuuint32_t estr[3] = {1, 1, 1};
+    const CUresult r = k1_encode_tiled()(&map, CU_TENSOR_MAP_DATA_TYPE_UINT32, 3, (void*)rgb, dims, strides, box,
+                                         estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                                         CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) {
+      set_error("cuTensorMapEncodeTiled failed for the RGB batch");
+      return MTB_ECUDA;
+    }
+  }
+  static bool attr_done = false;
+  if (!attr_done) {
+    MTB_CUDA(cudaFuncSetAttribute(pipe_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kPipeSmemBytes));
+    attr_done = true;
+  }
+  const int grid = num_sms();
+  int launches = 0;
+  for (int j = 0; j < J; ++j) {
+    a.j = j;
+    a.k1_img = j < n_img ? j : -1;
+    a.th_img = (j >= 1 && j <= n_img) ? j - 1 : -1;
+    a.n_items = 0;
+    a.search_tiles = 0;
+    for (int q = 0; q < n_pairs; ++q) {
+      const int d = j - ready[q];
+      if (d < 0 || d >= p.n) continue;
+      MTB_REQUIRE(a.n_items < kPipeMaxItems, "too many pairs in flight for one fused launch");
+      PipeItem& it = a.items[a.n_items++];
+      it.pair = q;
+      it.ref = pairs_host[2 * q];
+      it.tgt = pairs_host[2 * q + 1];
+      it.level = p.n - 1 - d;
+      it.tile0 = a.search_tiles;
+      a.search_tiles += search_tiles_level[it.level];
+    }
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3((unsigned)grid);
+    cfg.blockDim = dim3(kK1Threads);
+    cfg.dynamicSmemBytes = kPipeSmemBytes;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    const cudaError_t e = cudaLaunchKernelEx(&cfg, pipe_kernel, a, map);
+    if (e != cudaSuccess) {
+      set_error(std::string("pipe_kernel: ") + cudaGetErrorString(e));
+      return MTB_ECUDA;
+    }
+    ++launches;
+  }
+  return check_launch("pipe_kernel", launches);
+}

@@ -197,6 +197,60 @@ class MtbEngine:
             counters.bump(SHIFTED_ERROR_EVALS, 9 * self.n * n_pairs)
         return acc, errs
 
+    # ---------------------------------------------------------------- fused --
+    @property
+    def fused_supported(self) -> bool:
+        """True when the one-launch-per-image pipeline (csrc/pipe.cu) handles this geometry."""
+        return self.n <= 6 and (3 * self.width) % 16 == 0
+
+    def fused_workspace(self) -> dict:
+        """Scratch for align_fused: two gray slots (the pipeline keeps them L2-resident)."""
+        t = self.torch
+        ws = getattr(self, "_fused_ws", None)
+        if ws is None:
+            gb = np.zeros(1, dtype=np.int64)
+            _lib.load().mtb_align_fused_workspace(self.width, self.height, self.requested_levels,
+                                                  gb.ctypes.data_as(_lib._i64p), None)
+            ws = {"gray": t.empty(int(gb[0]), dtype=t.uint8, device="cuda")}
+            self._fused_ws = ws
+        return ws
+
+    def align_fused(self, rgb, pairs, pyr: PyramidSet | None = None, acc=None, errs=None, done=None,
+                    count: bool = True):
+        """Preprocess every image of `rgb` and find_offset every (ref, tgt) pair in ONE
+        software-pipelined sequence of launches (csrc/pipe.cu): pipeline.py:80-90
+        with search.py:74-95, gray pyramids kept in L2.  Returns (pyr, acc, errs)
+        with the same layouts as preprocess + search_table."""
+        t = self.torch
+        self._check_rgb(rgb)
+        if not self.fused_supported:
+            raise ValueError("fused path needs <= 6 pyramid levels and 3*W % 16 == 0")
+        n_img = int(rgb.shape[0])
+        pairs = np.ascontiguousarray(np.asarray(pairs, dtype=np.int32).reshape(-1, 2))
+        P = len(pairs)
+        if pyr is None:
+            pyr = self.alloc(n_img)
+        if acc is None:
+            acc = t.empty((max(P, 1), self.n, 2), dtype=t.int32, device="cuda")
+        if errs is None:
+            errs = t.empty((max(P, 1), self.n, 9), dtype=t.int64, device="cuda")
+        if done is None:
+            done = t.empty((max(P, 1), self.n), dtype=t.int32, device="cuda")
+        ws = self.fused_workspace()
+        sync = ws.get("sync")
+        if sync is None or sync.numel() < 17 * (n_img + 8):
+            sync = ws["sync"] = t.empty(17 * (n_img + 8), dtype=t.int32, device="cuda")
+        _lib.call("mtb_align_fused", _dev.ptr(rgb), 3 * self.width, 3 * self.width * self.height, self.width,
+                  self.height, n_img, self.requested_levels, self.tol, pairs.ctypes.data, P, _dev.ptr(ws["gray"]),
+                  _dev.ptr(pyr.hist_ws), _dev.ptr(pyr.medians), _dev.ptr(pyr.mtb), _dev.ptr(pyr.excl),
+                  _dev.ptr(acc), _dev.ptr(errs), _dev.ptr(done), _dev.ptr(sync), _dev.stream())
+        if count:
+            counters.bump(PYRAMID_BUILDS, n_img)
+            counters.bump(MTB_PYRAMID_BUILDS, n_img)
+            counters.bump(FIND_OFFSET_CALLS, P)
+            counters.bump(SHIFTED_ERROR_EVALS, 9 * self.n * P)
+        return pyr, acc[:P], errs[:P]
+
     def search(self, pyr: PyramidSet, pairs, count: bool = True):
         table = self.maps_table(pyr, pairs)
         return self.search_table(table, int(table.shape[1]), count=count)
