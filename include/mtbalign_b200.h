@@ -248,6 +248,31 @@ int mtb_decide_level(const unsigned long long* errs, int64_t errs_stride,
                      const int32_t* prev, int64_t prev_stride, const int32_t* base,
                      int32_t* acc, int64_t acc_stride, int P, void* stream);
 
+/* ------------------------------------------------------------------------ */
+/* 4. Fused pipeline — preprocess + find_offset of a whole batch            */
+/* ------------------------------------------------------------------------ */
+
+/* Workspace of mtb_align_fused for W x H images: *gray_bytes = the tile-major
+ * gray ring (3 image slots, kept L2-resident), *hist_elems = spread-histogram
+ * u32 per image.  Returns the level count, or -1 when the geometry needs the
+ * staged entry points (more than 6 levels).  sync_ws needs 17 * (n_img + 8)
+ * u32. */
+int mtb_align_fused_workspace(int w, int h, int levels, int64_t* gray_bytes, int64_t* hist_elems);
+
+/* pipeline.py:80-90 (to_grayscale -> build_pyramid -> build_mtb_pyramid for
+ * every image) followed by find_offset (search.py:74-95) for every pair in
+ * pairs_host [host, n_pairs x (ref, tgt)], as one software-pipelined
+ * sequence of n_img + 1 + levels launches (one image per launch, K1 / K3 /
+ * search of different images overlapped, gray never written to HBM).
+ * rgb: n_img images, 16-B aligned rows with 3*W % 16 == 0.  Outputs have the
+ * layouts of mtb_preprocess (medians, packed maps) and mtb_find_offset_batch
+ * (acc [P][n][2], errs [P][n][9], done [P][n] scratch).  Bit-identical to the
+ * staged entry points. */
+int mtb_align_fused(const uint8_t* rgb, int64_t rgb_pitch, int64_t rgb_img_stride, int w, int h, int n_img,
+                    int levels, int tol, const int32_t* pairs_host, int n_pairs, uint8_t* gray_ws,
+                    uint32_t* hist_ws, int32_t* medians, uint64_t* mtb, uint64_t* exclusion, int32_t* acc,
+                    unsigned long long* errs, uint32_t* done, uint32_t* sync_ws, void* stream);
+
 #ifdef __cplusplus
 }
 #endif
