@@ -62,6 +62,7 @@ struct PipeArgs {
   uint32_t* ctr;                     // [launch][16] aux task stripes, then [launch] K1 tile counters; zeroed
   int n_launch;
   int search_first;                  // aux task order (MTB_PIPE_SEARCH_FIRST)
+  int probe;                         // diagnostics (MTB_PIPE_PROBE): 1 = no K1 tiles, 2 = no aux tasks
   int j;                             // this launch's index
   int k1_img;                        // image of the K1 part, or -1
   int th_img;                        // image of the K3 part, or -1
@@ -98,10 +99,11 @@ struct SearchStage {
 struct PipeSmem {
   uint32_t hist[6][256];                                  // 1 KB-aligned levels (see k1_tile.cuh)
   uint8_t rgb[kPK1Groups][kPStages][kK1TileBytes];
-  SearchStage srch[kPAuxWarps];
+  uint8_t abuf[kPAuxWarps][2][4096];                      // aux warps: K3 double buffer / search staging
   uint8_t l3[kPK1Groups][2][4][32];
   unsigned long long full[kPK1Groups][kPStages];
   int tile_of[kPK1Groups][kPStages];                      // tile in each ring stage (-1: no more)
+  unsigned long long kbar[kPipeWarps][2];                 // per-warp K3 staging mbarriers
   ThConst th[kPipeMaxLevels];
   int last;
   int next;                                               // aux task queue head
@@ -296,6 +298,88 @@ __device__ __forceinline__ void k3_finish(const uint8_t* slot, uint32_t* mtb, ui
   }
 }
 
+// ---- K3 via TMA bulk copies ------------------------------------------------
+// Task r of level K (K <= 3) = bitmap words f0 = 128 r .. f0 + 127 in tile
+// order = 4 KB of tile-major gray made of pieces of min(128, words/tile) words
+// (L0: one 4 KB half-tile, L1: 2 x 2 KB, L2: 8 x 512 B, L3: 32 x 128 B).
+// Lane i copies piece i with cp.async.bulk into the warp's staging buffer;
+// the copy completes on the buffer's mbarrier, so a warp computes task r
+// while task r+1 is in flight, without holding it in registers.
+__device__ __forceinline__ void k3_bulk_issue(const PipeArgs& a, const uint8_t* slot, int K, int r, int lane,
+                                              uint8_t* buf, unsigned long long* bar) {
+  const int lwpt = 8 - 2 * K;
+  const int wpt = 1 << lwpt;
+  const int pw = wpt < 128 ? wpt : 128;          // words per piece
+  const int npieces = 128 / pw;
+  const int ntiles = a.g.tiles_x * a.g.tiles_y;
+  const int f0 = 128 * r;
+  // bytes that exist (pieces of tiles past the end are not copied)
+  const int tiles_needed = ((f0 + 127) >> lwpt) - (f0 >> lwpt) + 1;
+  int bytes = 4096;
+  if ((f0 >> lwpt) + tiles_needed > ntiles) {
+    const int last_f = ntiles << lwpt;                  // words that exist at this level
+    bytes = (last_f - f0) * 32;
+  }
+  if (lane == 0) mbar_expect_tx(bar, (uint32_t)bytes);
+  __syncwarp();
+  if (lane < npieces) {
+    const int f = f0 + lane * pw;
+    const int t = f >> lwpt;
+    if (t < ntiles) {
+      const uint8_t* src = slot + (int64_t)t * kTileGrayBytes + tm_off(K) + (f & (wpt - 1)) * 32;
+      asm volatile(
+          "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+              smem_addr(buf + lane * pw * 32)),
+          "l"(src), "r"(pw * 32), "r"(smem_addr(bar))
+          : "memory");
+    }
+  }
+}
+
+__device__ __forceinline__ void k3_bulk_finish(const PipeArgs& a, const uint8_t* slot, uint32_t* mtb, uint32_t* excl,
+                                               const ThConst* th, uint32_t yt, uint32_t ytl, int K, int r, int lane,
+                                               const uint8_t* buf, unsigned long long* bar, uint32_t parity) {
+  mbar_wait(bar, parity);
+  const int lwpr = 3 - K, wpr = 1 << lwpr;
+  const int lwpt = 8 - 2 * K, wpt = 1 << lwpt;
+  const int rows = kK1TileRows >> K;
+  const int ntiles = a.g.tiles_x * a.g.tiles_y;
+  const int nw = a.nw32[K], lh = a.g.lh[K], lw = a.g.lw[K];
+  const int boff = (int)a.bit_off32[K];
+  const ThConst c = th[K];
+  const int f0 = 128 * r;
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const int w = i * 32 + lane;
+    const int f = f0 + w;
+    const int t = f >> lwpt;
+    const int rem = f & (wpt - 1);
+    const int row = rem >> lwpr, cc = rem & (wpr - 1);
+    const int ty = div_tiles_x(a, t), tx = t - ty * a.g.tiles_x;
+    const int y = ty * rows + row, j = tx * wpr + cc;
+    const uint4 v0 = *reinterpret_cast<const uint4*>(buf + w * 32);
+    const uint4 v1 = *reinterpret_cast<const uint4*>(buf + w * 32 + 16);
+    const uint32_t g[8] = {v0.x, v0.y, v0.z, v0.w, v1.x, v1.y, v1.z, v1.w};
+    uint32_t m, e;
+    th_word(g, c, yt, ytl, lw - 32 * j, m, e);
+    if (t < ntiles && y < lh && j < nw) {
+      const int o = boff + y * nw + j;
+      mtb[o] = m;
+      excl[o] = e;
+    }
+  }
+  // line `lane` of the task's 4 KB: drop it from L2 without write-back
+  {
+    const int f = f0 + 4 * lane;
+    const int t = f >> lwpt;
+    if (t < ntiles)
+      asm volatile("discard.global.L2 [%0], 128;" ::"l"(slot + (int64_t)t * kTileGrayBytes + tm_off(K) +
+                                                         (f & (wpt - 1)) * 32)
+                   : "memory");
+  }
+  __syncwarp();   // the buffer may be refilled next
+}
+
 // 32 gray bytes of a level-4/5 word gathered from the tiles it spans
 // (K = 4: two 16-px tile rows, K = 5: four 8-px tile rows).
 template <int K>
@@ -484,7 +568,8 @@ __device__ __forceinline__ void pipe_search_flush(const PipeArgs& a, const PipeI
 // wait, the K1 warps once their tiles are done — so the CTA's K1 and aux
 // work finish together.
 constexpr int kAuxPhases = 7;
-static_assert(4 * sizeof(SearchStage) <= kK1TileBytes, "K1 warps stage search tiles in a ring stage");
+static_assert(sizeof(SearchStage) <= 8192, "search staging fits a warp's 2 x 4 KB K3 buffers");
+static_assert(kPStages * kK1TileBytes >= 4 * 16384, "K1 warps stage in their group ring");
 
 struct AuxCtx {
   const uint8_t* slot;
@@ -492,7 +577,9 @@ struct AuxCtx {
   uint32_t* excl;
   uint32_t yt, ytl;
   int lane;
-  SearchStage* stage;
+  SearchStage* stage;          // search staging (aliases kbuf)
+  uint8_t* kbuf;               // 2 x 4 KB K3 staging
+  unsigned long long* kbar;    // its 2 mbarriers
   bool tracer;   // diagnostics: this warp stamps phase starts (MTB_PIPE_TRACE)
 };
 
@@ -570,7 +657,7 @@ __device__ __forceinline__ int aux_phase_of(const PipeArgs& a, int q) {
   return a.search_first ? (q == 0 ? 6 : q - 1) : q;
 }
 
-__device__ __noinline__ void aux_drain(const PipeArgs& a, PipeSmem& S, const AuxCtx& x) {
+__device__ __forceinline__ void aux_drain(const PipeArgs& a, PipeSmem& S, const AuxCtx& x) {
   const int G = gridDim.x, c = blockIdx.x;
   int lo[kAuxPhases], cnt[kAuxPhases];
 #pragma unroll
@@ -579,15 +666,23 @@ __device__ __noinline__ void aux_drain(const PipeArgs& a, PipeSmem& S, const Aux
     lo[q] = (int)((int64_t)c * T / G);
     cnt[q] = (int)((int64_t)(c + 1) * T / G) - lo[q];
   }
+  if (x.lane == 0) {
+    mbar_init(&x.kbar[0], 1);
+    mbar_init(&x.kbar[1], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncwarp();
+  uint32_t par[2] = {0u, 0u};
+  int pend_k = -1, pend_r = 0, pend_b = 0;   // K3 task in flight
+  int nb = 0;                                // next staging buffer
   for (;;) {
     int t = 0;
     if (x.lane == 0) t = atomicAdd(&S.next, 1);
     t = __shfl_sync(0xffffffffu, t, 0);
     int q = 0;
     while (q < kAuxPhases && t >= cnt[q]) t -= cnt[q++];
-    if (q == kAuxPhases) return;
-    const int p = aux_phase_of(a, q);
-    if (x.tracer && x.lane == 0 && a.trace) {
+    const int p = q < kAuxPhases ? aux_phase_of(a, q) : -1;
+    if (p >= 0 && x.tracer && x.lane == 0 && a.trace) {
       unsigned long long* slot = a.trace + ((int64_t)a.j * gridDim.x + blockIdx.x) * 16 + 8 + p;
       if (*slot == 0) {
         unsigned long long tt;
@@ -595,13 +690,27 @@ __device__ __noinline__ void aux_drain(const PipeArgs& a, PipeSmem& S, const Aux
         *slot = tt;
       }
     }
-    if (p < 4) {
-      K3Task T;
-      k3_issue(a, x.slot, p, 4 * (lo[q] + t), x.lane, T);
-      k3_finish(x.slot, x.mtb, x.excl, S.th, x.yt, x.ytl, T, x.lane);
-    } else {
-      aux_run(a, S, x, p, lo[q] + t);
+    if (p >= 0 && p < 4) {
+      k3_bulk_issue(a, x.slot, p, lo[q] + t, x.lane, x.kbuf + nb * 4096, &x.kbar[nb]);
+      if (pend_k >= 0) {
+        k3_bulk_finish(a, x.slot, x.mtb, x.excl, S.th, x.yt, x.ytl, pend_k, pend_r, x.lane, x.kbuf + pend_b * 4096,
+                       &x.kbar[pend_b], par[pend_b]);
+        par[pend_b] ^= 1u;
+      }
+      pend_k = p;
+      pend_r = lo[q] + t;
+      pend_b = nb;
+      nb ^= 1;
+      continue;
     }
+    if (pend_k >= 0) {
+      k3_bulk_finish(a, x.slot, x.mtb, x.excl, S.th, x.yt, x.ytl, pend_k, pend_r, x.lane, x.kbuf + pend_b * 4096,
+                     &x.kbar[pend_b], par[pend_b]);
+      par[pend_b] ^= 1u;
+      pend_k = -1;
+    }
+    if (p < 0) return;
+    aux_run(a, S, x, p, lo[q] + t);
   }
 }
 
@@ -629,7 +738,7 @@ __global__ void __launch_bounds__(kK1Threads, 1) pipe_kernel(const __grid_consta
     const int kt = tid;               // 0..255 among the K1 threads
     const uint32_t hb = smem_addr(&S.hist[0][0]);
     stamp(0);
-    if (a.k1_img >= 0) {
+    if (a.k1_img >= 0 && a.probe != 1) {
       const int tiles_img = a.g.tiles_x * a.g.tiles_y;
       uint32_t* ctr = a.ctr + a.j;   // K1 tile counter of this launch
       uint64_t pol_first;
@@ -727,46 +836,33 @@ __global__ void __launch_bounds__(kK1Threads, 1) pipe_kernel(const __grid_consta
     grid_dep_wait();
     grid_dep_launch();
     asm volatile("bar.sync 9, %0;" ::"r"(kK1Threads) : "memory");   // S.th / S.next ready
-    AuxCtx ax;
-    ax.slot = a.g.gray + (int64_t)((a.th_img >= 0 ? a.th_img : 0) % kPGraySlots) * a.g.gray_img_stride;
-    ax.mtb = a.mtb + (int64_t)(a.th_img >= 0 ? a.th_img : 0) * a.bit_img_words32;
-    ax.excl = a.excl + (int64_t)(a.th_img >= 0 ? a.th_img : 0) * a.bit_img_words32;
-    ax.yt = (uint32_t)(255 - a.tol) * 0x01010101u;
-    ax.ytl = ax.yt & 0x7f7f7f7fu;
-    ax.lane = lane;
-    // search staging in this group's first ring stage (all its TMA copies have landed)
-    ax.stage = reinterpret_cast<SearchStage*>(&S.rgb[warp >> 2][0][0]) + (warp & 3);
-    ax.tracer = true;
-    aux_drain(a, S, ax);
-    stamp(3);
-    named_bar(10, kK1Threads);   // every task of this CTA done
-    return;
+  } else {
+    // ======================= aux warps: K3 + search ==========================
+    const int at = tid - 32 * kPK1Warps;    // 0..255
+    grid_dep_wait();                         // launch j-1 (and so all earlier) complete
+    grid_dep_launch();
+    stamp(4);
+    if (a.trace && at == 0) {
+      unsigned smid;
+      asm volatile("mov.u32 %0, %smid;" : "=r"(smid));
+      a.trace[((int64_t)a.j * gridDim.x + blockIdx.x) * 16 + 6] = smid;
+    }
+    if (a.th_img >= 0 && at < a.n) {
+      const int med = __ldcg(a.medians + a.th_img * a.n + at);
+      ThConst c;
+      c.med = (uint32_t)med * 0x01010101u;
+      c.ym = (uint32_t)(255 - med) * 0x01010101u;
+      c.yml = c.ym & 0x7f7f7f7fu;
+      c.med_lo = med <= 127;
+      S.th[at] = c;
+    }
+    if (at == 0) S.next = 0;
+    for (int i = at; i < a.n_items * 9; i += 32 * kPAuxWarps) (&S.scnt[0][0])[i] = 0;
+    named_bar(6, 32 * kPAuxWarps);
+    asm volatile("bar.arrive 9, %0;" ::"r"(kK1Threads) : "memory");
   }
 
-  // ========================= aux warps: K3 + search ==========================
-  const int aw = warp - kPK1Warps;
-  const int at = tid - 32 * kPK1Warps;    // 0..255
-  grid_dep_wait();                         // launch j-1 (and so all earlier) complete
-  grid_dep_launch();
-  stamp(4);
-  if (a.trace && at == 0) {
-    unsigned smid;
-    asm volatile("mov.u32 %0, %smid;" : "=r"(smid));
-    a.trace[((int64_t)a.j * gridDim.x + blockIdx.x) * 16 + 6] = smid;
-  }
-  if (a.th_img >= 0 && at < a.n) {
-    const int med = __ldcg(a.medians + a.th_img * a.n + at);
-    ThConst c;
-    c.med = (uint32_t)med * 0x01010101u;
-    c.ym = (uint32_t)(255 - med) * 0x01010101u;
-    c.yml = c.ym & 0x7f7f7f7fu;
-    c.med_lo = med <= 127;
-    S.th[at] = c;
-  }
-  if (at == 0) S.next = 0;
-  for (int i = at; i < a.n_items * 9; i += 32 * kPAuxWarps) (&S.scnt[0][0])[i] = 0;
-  named_bar(6, 32 * kPAuxWarps);
-  asm volatile("bar.arrive 9, %0;" ::"r"(kK1Threads) : "memory");
+  // ============ every warp: this CTA's share of the aux tasks ================
   AuxCtx ax;
   ax.slot = a.g.gray + (int64_t)((a.th_img >= 0 ? a.th_img : 0) % kPGraySlots) * a.g.gray_img_stride;
   ax.mtb = a.mtb + (int64_t)(a.th_img >= 0 ? a.th_img : 0) * a.bit_img_words32;
@@ -774,12 +870,19 @@ __global__ void __launch_bounds__(kK1Threads, 1) pipe_kernel(const __grid_consta
   ax.yt = (uint32_t)(255 - a.tol) * 0x01010101u;
   ax.ytl = ax.yt & 0x7f7f7f7fu;
   ax.lane = lane;
-  ax.stage = &S.srch[aw];
+  // K1 warps stage in their group's ring (all its TMA copies have landed,
+  // 16 KB per warp); aux warps in their own 8 KB
+  ax.kbuf = warp < kPK1Warps
+                ? &S.rgb[0][0][0] + (size_t)(warp >> 2) * (kPStages * kK1TileBytes) + (warp & 3) * 16384
+                : &S.abuf[warp - kPK1Warps][0][0];
+  ax.kbar = S.kbar[warp];
+  ax.stage = reinterpret_cast<SearchStage*>(ax.kbuf);
   ax.tracer = true;
-  aux_drain(a, S, ax);
-  stamp(5);
-  named_bar(10, kK1Threads);
-  if (at < a.n_items) pipe_search_flush(a, a.items[at], S.scnt[at]);
+  if (a.probe != 2) aux_drain(a, S, ax);
+  stamp(warp < kPK1Warps ? 3 : 5);
+  named_bar(10, kK1Threads);   // every task of this CTA done
+  const int ft = tid - 32 * kPK1Warps;
+  if (ft >= 0 && ft < a.n_items) pipe_search_flush(a, a.items[ft], S.scnt[ft]);
 }
 
 bool k1_rgb_supported(int w, int64_t rgb_pitch, int64_t rgb_img_stride, const void* rgb);
@@ -872,6 +975,8 @@ extern "C" int mtb_align_fused(const uint8_t* rgb, int64_t rgb_pitch, int64_t rg
   a.bit_img_words32 = 2 * p.bit_img_words;
   a.medians = medians;
   {
+    const char* pr = getenv("MTB_PIPE_PROBE");
+    a.probe = pr ? atoi(pr) : 0;
     const char* sf = getenv("MTB_PIPE_SEARCH_FIRST");
     a.search_first = sf ? atoi(sf) : 0;
     const char* tr = getenv("MTB_PIPE_TRACE");   // device address of a [J][grid][8] u64 buffer

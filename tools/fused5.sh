@@ -1,5 +1,5 @@
 timeout 600 python -m pytest tests/test_gpu_fused.py -x -q 2>&1 | grep -E "passed|failed|Error|assert" | head -8
-B="python bench.py --steps 1 --warmup 3 --no-graph --no-cpu-baseline --no-e2e --pairs 8"
+B="python bench.py --steps 1 --warmup 3 --no-graph --no-cpu-baseline --no-e2e --pairs 8 --mode fused"
 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum,lts__t_sectors_srcunit_tex_op_read_lookup_hit.sum,lts__t_sectors_srcunit_tex_op_read_lookup_miss.sum --cache-control none --clock-control none -k regex:pipe -s 25 -c 6 --csv --log-file gpurun_out/pipe_nf.csv $B > /dev/null 2>&1
 python - <<'PY'
 import csv

@@ -1,5 +1,5 @@
 timeout 600 python -m pytest tests/test_gpu_fused.py -x -q 2>&1 | grep -E "passed|failed|Error|assert" | head -8
-for sf in 0 1; do
-MTB_PIPE_SEARCH_FIRST=$sf timeout 300 python bench.py --steps 50 --no-cpu-baseline --no-e2e 2>&1 | tail -1 | python -c 'import json,sys; d=json.loads(sys.stdin.read()); print("search_first='$sf' value", d["value"], "ms", d["ms_per_step"], d["config"]["correct_offsets"])'
+for sf in 0; do
+MTB_PIPE_SEARCH_FIRST=$sf timeout 300 python bench.py --mode fused --steps 50 --no-cpu-baseline --no-e2e 2>&1 | tail -1 | python -c 'import json,sys; d=json.loads(sys.stdin.read()); print("search_first='$sf' value", d["value"], "ms", d["ms_per_step"], d["config"]["correct_offsets"])'
 done
 python tools/pipe_trace.py 2>&1 | sed -n '5,45p' | awk 'NR%3==1'
