@@ -255,9 +255,13 @@ int mtb_decide_level(const unsigned long long* errs, int64_t errs_stride,
 /* Workspace of mtb_align_fused for W x H images: *gray_bytes = the tile-major
  * gray ring (3 image slots, kept L2-resident), *hist_elems = spread-histogram
  * u32 per image.  Returns the level count, or -1 when the geometry needs the
- * staged entry points (more than 6 levels).  sync_ws needs 17 * (n_img + 8)
- * u32. */
+ * staged entry points (more than 6 levels). */
 int mtb_align_fused_workspace(int w, int h, int levels, int64_t* gray_bytes, int64_t* hist_elems);
+
+/* u32 words of the sync_ws scratch of mtb_align_fused: per-launch tile
+ * counters, per-image medians-ready flags and threshold-done counters, and
+ * per-(pair, level) decided flags (zeroed by the call). */
+int64_t mtb_align_fused_sync_words(int n_img, int n_pairs, int levels);
 
 /* pipeline.py:80-90 (to_grayscale -> build_pyramid -> build_mtb_pyramid for
  * every image) followed by find_offset (search.py:74-95) for every pair in

@@ -70,6 +70,7 @@ AUX_SIGNATURES = {
     "mtb_launch_count": ([], ctypes.c_uint64),
     "mtb_plan_levels": ([_i32, _i32, _i32, _i64p, _i64p], ctypes.c_int),
     "mtb_align_fused_workspace": ([_i32, _i32, _i32, _i64p, _i64p], ctypes.c_int),
+    "mtb_align_fused_sync_words": ([_i32, _i32, _i32], ctypes.c_int64),
 }
 
 _lock = threading.Lock()

@@ -59,7 +59,10 @@ struct PipeArgs {
   int32_t* acc;                      // [P][n][2]
   unsigned long long* errs;          // [P][n][9]
   uint32_t* done;                    // [P][n]
-  uint32_t* ctr;                     // [launch][16] aux task stripes, then [launch] K1 tile counters; zeroed
+  uint32_t* ctr;                     // [launch] K1 tile counters (zeroed)
+  uint32_t* med_ready;               // [img] 1 once the image's medians (and all its gray) are published
+  uint32_t* k3_done;                 // [img] CTAs that finished thresholding the image
+  uint32_t* decided;                 // [P][n] 1 once the (pair, level) offset is published
   int n_launch;
   int search_first;                  // aux task order (MTB_PIPE_SEARCH_FIRST)
   int probe;                         // diagnostics (MTB_PIPE_PROBE): 1 = no K1 tiles, 2 = no aux tasks
@@ -88,6 +91,7 @@ constexpr int kPK1Warps = 4 * kPK1Groups;
 constexpr int kPAuxWarps = kPipeWarps - kPK1Warps;
 constexpr int kPStages = 3;
 constexpr int kPGraySlots = 3;
+constexpr int kAuxPhases = 7;     // aux task phases: K3 levels 0..3, levels 4..5, padding, search
 
 // Per-aux-warp staging of one search warp-tile: 8 output rows x 32 words of
 // the reference maps, 10 source rows x 35 words of the target maps.
@@ -107,12 +111,29 @@ struct PipeSmem {
   ThConst th[kPipeMaxLevels];
   int last;
   int next;                                               // aux task queue head
+  int plo[kAuxPhases], pcnt[kAuxPhases];                  // this CTA's slice of each aux phase
   unsigned scnt[kPipeMaxItems][9];                        // per-item partial search counts
 };
 constexpr int kPipeSmemBytes = (int)sizeof(PipeSmem) + 1024;
 
 __device__ __forceinline__ void grid_dep_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 __device__ __forceinline__ void grid_dep_launch() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+
+// Cross-launch dependencies are flags in global memory (release: fence +
+// atomic; acquire: ld.acquire.gpu), not whole-grid waits: launch j+1's aux
+// work starts as soon as image j's K1 is published, while launch j's aux
+// work may still run on other SMs.  Every flag is produced by a launch whose
+// CTAs are all resident once its successor runs (a launch can only start
+// after every CTA of its predecessor has started), so spinning cannot
+// deadlock.
+__device__ __forceinline__ uint32_t ld_acquire(const uint32_t* p) {
+  uint32_t v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void spin_geq(const uint32_t* p, uint32_t v) {
+  while (ld_acquire(p) < v) __nanosleep(100);
+}
 
 // Lower median of one level's spread histogram (threshold.py:31-39): the
 // smallest m with cumsum[m] >= (total + 1) / 2.  One warp; lane owns 8 bins.
@@ -152,6 +173,34 @@ __device__ __forceinline__ int warp_median(const uint32_t* spread, int lane) {
 //   excl : |g - med| > tol       — d = VABSDIFF4(g, med); carry-out of d + (255 - tol)
 // With the per-level bit 7 of the addend known, MAJ is one LOP3 that also
 // masks bit 7; the four flags of a word are gathered by one multiply.
+// MED_LO: bit 7 of (255 - median) is set, so the MTB carry MAJ(x7, 1, s7)
+// is (x | s) bit 7 — one LOP3 with the mask; else MAJ(x7, 0, s7) = x & s.
+// The exclusion compare assumes tol <= 127 (the carry is (d | sd) bit 7);
+// larger tolerances take the generic majority form.
+template <bool MED_LO, bool TOL_LO>
+__device__ __forceinline__ void th_word_t(const uint32_t (&g)[8], const ThConst& c, uint32_t yt, uint32_t ytl,
+                                          int valid, uint32_t& mw, uint32_t& ew) {
+  constexpr uint32_t H = 0x80808080u, L7 = 0x7f7f7f7fu;
+  uint32_t m = 0, e = 0;
+#pragma unroll
+  for (int k = 0; k < 8; ++k) {
+    const uint32_t x = g[k];
+    const uint32_t s = (x & L7) + c.yml;
+    const uint32_t gm = MED_LO ? ((x | s) & H) : (x & s & H);       // byte carry-out of x + (255 - med)
+    uint32_t d;
+    asm("vabsdiff4.u32.u32.u32 %0, %1, %2, %3;" : "=r"(d) : "r"(x), "r"(c.med), "r"(0u));
+    const uint32_t sd = (d & L7) + ytl;
+    const uint32_t ge = TOL_LO ? ((d | sd) & H) : (((d & yt) | (d & sd) | (yt & sd)) & H);   // |x - med| > tol
+    // flags at bits 7,15,23,31 -> bits 28..31 of the product -> bits 4k..4k+3
+    m = (((gm * 0x00204081u) >> (28 - 4 * k)) & (0xfu << (4 * k))) | m;
+    e = (((ge * 0x00204081u) >> (28 - 4 * k)) & (0xfu << (4 * k))) | e;
+  }
+  const uint32_t keep = valid >= 32 ? 0xffffffffu : (valid <= 0 ? 0u : ((1u << valid) - 1u));
+  mw = m & keep;
+  ew = e & keep;
+}
+
+// Generic form (any median, any tolerance): full majority for both carries.
 __device__ __forceinline__ void th_word(const uint32_t (&g)[8], const ThConst& c, uint32_t yt, uint32_t ytl,
                                         int valid, uint32_t& mw, uint32_t& ew) {
   constexpr uint32_t H = 0x80808080u, L7 = 0x7f7f7f7fu;
@@ -160,12 +209,11 @@ __device__ __forceinline__ void th_word(const uint32_t (&g)[8], const ThConst& c
   for (int k = 0; k < 8; ++k) {
     const uint32_t x = g[k];
     const uint32_t s = (x & L7) + c.yml;
-    const uint32_t gm = ((x & c.ym) | (x & s) | (c.ym & s)) & H;      // MAJ: byte carry-out of x + (255 - med)
+    const uint32_t gm = ((x & c.ym) | (x & s) | (c.ym & s)) & H;
     uint32_t d;
     asm("vabsdiff4.u32.u32.u32 %0, %1, %2, %3;" : "=r"(d) : "r"(x), "r"(c.med), "r"(0u));
     const uint32_t sd = (d & L7) + ytl;
-    const uint32_t ge = ((d & yt) | (d & sd) | (yt & sd)) & H;        // carry-out of |x - med| + (255 - tol)
-    // flags at bits 7,15,23,31 -> bits 28..31 of the product -> bits 4k..4k+3
+    const uint32_t ge = ((d & yt) | (d & sd) | (yt & sd)) & H;
     m = (((gm * 0x00204081u) >> (28 - 4 * k)) & (0xfu << (4 * k))) | m;
     e = (((ge * 0x00204081u) >> (28 - 4 * k)) & (0xfu << (4 * k))) | e;
   }
@@ -336,17 +384,15 @@ __device__ __forceinline__ void k3_bulk_issue(const PipeArgs& a, const uint8_t* 
   }
 }
 
-__device__ __forceinline__ void k3_bulk_finish(const PipeArgs& a, const uint8_t* slot, uint32_t* mtb, uint32_t* excl,
-                                               const ThConst* th, uint32_t yt, uint32_t ytl, int K, int r, int lane,
-                                               const uint8_t* buf, unsigned long long* bar, uint32_t parity) {
-  mbar_wait(bar, parity);
+template <bool MED_LO>
+__device__ __forceinline__ void k3_bulk_units(const PipeArgs& a, uint32_t* mtb, uint32_t* excl, const ThConst& c,
+                                              uint32_t yt, uint32_t ytl, int K, int r, int lane, const uint8_t* buf) {
   const int lwpr = 3 - K, wpr = 1 << lwpr;
   const int lwpt = 8 - 2 * K, wpt = 1 << lwpt;
   const int rows = kK1TileRows >> K;
   const int ntiles = a.g.tiles_x * a.g.tiles_y;
   const int nw = a.nw32[K], lh = a.g.lh[K], lw = a.g.lw[K];
   const int boff = (int)a.bit_off32[K];
-  const ThConst c = th[K];
   const int f0 = 128 * r;
 #pragma unroll
   for (int i = 0; i < 4; ++i) {
@@ -361,16 +407,51 @@ __device__ __forceinline__ void k3_bulk_finish(const PipeArgs& a, const uint8_t*
     const uint4 v1 = *reinterpret_cast<const uint4*>(buf + w * 32 + 16);
     const uint32_t g[8] = {v0.x, v0.y, v0.z, v0.w, v1.x, v1.y, v1.z, v1.w};
     uint32_t m, e;
-    th_word(g, c, yt, ytl, lw - 32 * j, m, e);
+    th_word_t<MED_LO, true>(g, c, yt, ytl, lw - 32 * j, m, e);
     if (t < ntiles && y < lh && j < nw) {
       const int o = boff + y * nw + j;
       mtb[o] = m;
       excl[o] = e;
     }
   }
+}
+
+__device__ __forceinline__ void k3_bulk_finish(const PipeArgs& a, const uint8_t* slot, uint32_t* mtb, uint32_t* excl,
+                                               const ThConst* th, uint32_t yt, uint32_t ytl, int K, int r, int lane,
+                                               const uint8_t* buf, unsigned long long* bar, uint32_t parity) {
+  mbar_wait(bar, parity);
+  const ThConst c = th[K];
+  if (a.tol > 127) {
+    // rare: generic majority for the exclusion compare
+    const int f0 = 128 * r;
+    for (int i = 0; i < 4; ++i) {
+      const int w = i * 32 + lane, f = f0 + w;
+      const int lwpr = 3 - K, lwpt = 8 - 2 * K;
+      const int t = f >> lwpt, rem = f & ((1 << lwpt) - 1);
+      const int row = rem >> lwpr, cc = rem & ((1 << lwpr) - 1);
+      const int ty = div_tiles_x(a, t), tx = t - ty * a.g.tiles_x;
+      const int y = ty * (kK1TileRows >> K) + row, j = tx * (1 << lwpr) + cc;
+      const uint4 v0 = *reinterpret_cast<const uint4*>(buf + w * 32);
+      const uint4 v1 = *reinterpret_cast<const uint4*>(buf + w * 32 + 16);
+      const uint32_t g[8] = {v0.x, v0.y, v0.z, v0.w, v1.x, v1.y, v1.z, v1.w};
+      uint32_t m, e;
+      th_word(g, c, yt, ytl, a.g.lw[K] - 32 * j, m, e);
+      if (t < a.g.tiles_x * a.g.tiles_y && y < a.g.lh[K] && j < a.nw32[K]) {
+        const int o = (int)a.bit_off32[K] + y * a.nw32[K] + j;
+        mtb[o] = m;
+        excl[o] = e;
+      }
+    }
+  } else if (c.med_lo) {
+    k3_bulk_units<true>(a, mtb, excl, c, yt, ytl, K, r, lane, buf);
+  } else {
+    k3_bulk_units<false>(a, mtb, excl, c, yt, ytl, K, r, lane, buf);
+  }
+  const int lwpt = 8 - 2 * K, wpt = 1 << lwpt;
+  const int ntiles = a.g.tiles_x * a.g.tiles_y;
   // line `lane` of the task's 4 KB: drop it from L2 without write-back
   {
-    const int f = f0 + 4 * lane;
+    const int f = 128 * r + 4 * lane;
     const int t = f >> lwpt;
     if (t < ntiles)
       asm volatile("discard.global.L2 [%0], 128;" ::"l"(slot + (int64_t)t * kTileGrayBytes + tm_off(K) +
@@ -427,6 +508,15 @@ __device__ __forceinline__ void pipe_search_tile(const PipeArgs& a, const PipeIt
   const int y0 = rb * 8;
   const int j0 = cb * 32;
   const int n = a.n;
+  if (lane == 0) {
+    if (k + 1 < n) {
+      spin_geq(a.decided + (int64_t)it.pair * n + (k + 1), 1u);
+    } else {
+      spin_geq(a.k3_done + it.ref, gridDim.x);
+      spin_geq(a.k3_done + it.tgt, gridDim.x);
+    }
+  }
+  __syncwarp();
   int bx = 0, by = 0;
   if (k + 1 < n) {
     const int32_t* prev = a.acc + ((int64_t)it.pair * n + (k + 1)) * 2;
@@ -543,6 +633,7 @@ __device__ __forceinline__ void pipe_search_flush(const PipeArgs& a, const PipeI
     __threadfence();
     int bx = 0, by = 0;
     if (k + 1 < n) {
+      spin_geq(a.decided + (int64_t)it.pair * n + (k + 1), 1u);
       const int32_t* prev = a.acc + ((int64_t)it.pair * n + (k + 1)) * 2;
       bx = 2 * __ldcg(prev);
       by = 2 * __ldcg(prev + 1);
@@ -557,6 +648,8 @@ __device__ __forceinline__ void pipe_search_flush(const PipeArgs& a, const PipeI
     int32_t* out = a.acc + ((int64_t)it.pair * n + k) * 2;
     out[0] = bx + best % 3 - 1;
     out[1] = by + best / 3 - 1;
+    __threadfence();
+    atomicExch(a.decided + (int64_t)it.pair * n + k, 1u);
   }
 }
 
@@ -567,7 +660,6 @@ __device__ __forceinline__ void pipe_search_flush(const PipeArgs& a, const PipeI
 // shared-memory counter — the aux warps right after the grid dependency
 // wait, the K1 warps once their tiles are done — so the CTA's K1 and aux
 // work finish together.
-constexpr int kAuxPhases = 7;
 static_assert(sizeof(SearchStage) <= 8192, "search staging fits a warp's 2 x 4 KB K3 buffers");
 static_assert(kPStages * kK1TileBytes >= 4 * 16384, "K1 warps stage in their group ring");
 
@@ -658,13 +750,11 @@ __device__ __forceinline__ int aux_phase_of(const PipeArgs& a, int q) {
 }
 
 __device__ __forceinline__ void aux_drain(const PipeArgs& a, PipeSmem& S, const AuxCtx& x) {
-  const int G = gridDim.x, c = blockIdx.x;
-  int lo[kAuxPhases], cnt[kAuxPhases];
+  int lo[kAuxPhases], cnt[kAuxPhases];   // this CTA's slices (computed once per CTA, aux prologue)
 #pragma unroll
   for (int q = 0; q < kAuxPhases; ++q) {
-    const int T = aux_phase_tasks(a, aux_phase_of(a, q));
-    lo[q] = (int)((int64_t)c * T / G);
-    cnt[q] = (int)((int64_t)(c + 1) * T / G) - lo[q];
+    lo[q] = S.plo[q];
+    cnt[q] = S.pcnt[q];
   }
   if (x.lane == 0) {
     mbar_init(&x.kbar[0], 1);
@@ -722,6 +812,9 @@ __global__ void __launch_bounds__(kK1Threads, 1) pipe_kernel(const __grid_consta
   const int tid = threadIdx.x;
   const int lane = tid & 31;
   const int warp = tid >> 5;
+  // All dependencies on earlier launches are explicit flags, so the next
+  // launch may be scheduled as soon as this one's CTAs are all resident.
+  grid_dep_launch();
   auto stamp = [&](int i) {
     if (a.trace && (tid & 255) == 0) {
       unsigned long long t;
@@ -765,7 +858,10 @@ __global__ void __launch_bounds__(kK1Threads, 1) pipe_kernel(const __grid_consta
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
         for (int s = 0; s < kPStages; ++s) claim(s);
       }
-      named_bar(5, 32 * kPK1Warps);   // hist zeroed, mbarriers initialised
+      // gray slot k1_img % 3 last held image k1_img - 3: wait until every CTA
+      // has thresholded it
+      if (kt == 0 && a.k1_img >= kPGraySlots) spin_geq(a.k3_done + (a.k1_img - kPGraySlots), gridDim.x);
+      named_bar(5, 32 * kPK1Warps);   // hist zeroed, mbarriers initialised, slot free
       uint8_t* slot = a.g.gray + (int64_t)(a.k1_img % kPGraySlots) * a.g.gray_img_stride;
       int k = 0, ptx = 0, pty = 0, ptile = 0;
       bool pfull = true;
@@ -828,19 +924,21 @@ __global__ void __launch_bounds__(kK1Threads, 1) pipe_kernel(const __grid_consta
           const int m = warp_median(gh + warp * 256 * kHistStrideK1, lane);
           if (lane == 0) a.medians[a.k1_img * a.n + warp] = m;
         }
+        named_bar(5, 32 * kPK1Warps);
+        if (kt == 0) {
+          __threadfence();
+          atomicExch(a.med_ready + a.k1_img, 1u);
+        }
       }
       stamp(2);
     }
-    // Join the aux work.  The wait also orders the trigger: launch j+1's K1
-    // overwrites the gray slot of image j-2, which launch j-1 reads.
-    grid_dep_wait();
-    grid_dep_launch();
+    // Join the aux work.
     asm volatile("bar.sync 9, %0;" ::"r"(kK1Threads) : "memory");   // S.th / S.next ready
   } else {
     // ======================= aux warps: K3 + search ==========================
     const int at = tid - 32 * kPK1Warps;    // 0..255
-    grid_dep_wait();                         // launch j-1 (and so all earlier) complete
-    grid_dep_launch();
+    if (at == 0 && a.th_img >= 0) spin_geq(a.med_ready + a.th_img, 1u);   // image th_img's K1 published
+    named_bar(6, 32 * kPAuxWarps);
     stamp(4);
     if (a.trace && at == 0) {
       unsigned smid;
@@ -857,6 +955,12 @@ __global__ void __launch_bounds__(kK1Threads, 1) pipe_kernel(const __grid_consta
       S.th[at] = c;
     }
     if (at == 0) S.next = 0;
+    if (at < kAuxPhases) {
+      const int G = gridDim.x, c = blockIdx.x;
+      const int T = aux_phase_tasks(a, aux_phase_of(a, at));
+      S.plo[at] = (int)((int64_t)c * T / G);
+      S.pcnt[at] = (int)((int64_t)(c + 1) * T / G) - S.plo[at];
+    }
     for (int i = at; i < a.n_items * 9; i += 32 * kPAuxWarps) (&S.scnt[0][0])[i] = 0;
     named_bar(6, 32 * kPAuxWarps);
     asm volatile("bar.arrive 9, %0;" ::"r"(kK1Threads) : "memory");
@@ -881,6 +985,10 @@ __global__ void __launch_bounds__(kK1Threads, 1) pipe_kernel(const __grid_consta
   if (a.probe != 2) aux_drain(a, S, ax);
   stamp(warp < kPK1Warps ? 3 : 5);
   named_bar(10, kK1Threads);   // every task of this CTA done
+  if (tid == 0 && a.th_img >= 0) {
+    __threadfence();
+    atomicAdd(a.k3_done + a.th_img, 1u);
+  }
   const int ft = tid - 32 * kPK1Warps;
   if (ft >= 0 && ft < a.n_items) pipe_search_flush(a, a.items[ft], S.scnt[ft]);
 }
@@ -892,6 +1000,10 @@ int64_t spread_hist_elems(int n_levels);
 }  // namespace mtb
 
 using namespace mtb;
+
+extern "C" int64_t mtb_align_fused_sync_words(int n_img, int n_pairs, int levels) {
+  return (int64_t)(n_img + 8) + 2 * (int64_t)n_img + (int64_t)n_pairs * (levels < 1 ? 1 : levels);
+}
 
 extern "C" int mtb_align_fused_workspace(int w, int h, int levels, int64_t* gray_bytes, int64_t* hist_elems) {
   Plan p;
@@ -1001,9 +1113,15 @@ extern "C" int mtb_align_fused(const uint8_t* rgb, int64_t rgb_pitch, int64_t rg
     ready[q] = (r > tg ? r : tg) + 2;
     if (ready[q] + p.n > J) J = ready[q] + p.n;
   }
-  // sync_ws: 17 counters per launch (mtb_align_fused_workspace: 17 * (n_img + 8) words)
+  // sync_ws (mtb_align_fused_sync_words): [J] K1 tile counters, [n_img]
+  // medians-ready flags, [n_img] K3-done counters, [P][n] decided flags
   MTB_REQUIRE(J <= n_img + 8, "internal: launch count");
-  MTB_CUDA(cudaMemsetAsync(sync_ws, 0, sizeof(uint32_t) * 17 * J, st));
+  const int64_t sync_words = (int64_t)(n_img + 8) + 2 * (int64_t)n_img + (int64_t)n_pairs * p.n;
+  MTB_CUDA(cudaMemsetAsync(sync_ws, 0, sizeof(uint32_t) * sync_words, st));
+  a.ctr = sync_ws;
+  a.med_ready = sync_ws + n_img + 8;
+  a.k3_done = a.med_ready + n_img;
+  a.decided = a.k3_done + n_img;
   a.n_launch = J;
   int search_tiles_level[kPipeMaxLevels];
   for (int k = 0; k < p.n; ++k) search_tiles_level[k] = ((p.lv[k].h + 7) / 8) * ((a.nw32[k] + 31) / 32);
@@ -1056,7 +1174,7 @@ extern "C" int mtb_align_fused(const uint8_t* rgb, int64_t rgb_pitch, int64_t rg
     attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
     attr[0].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = attr;
-    cfg.numAttrs = 1;
+    cfg.numAttrs = j > 0 ? 1 : 0;   // launch 0 follows the memsets in full stream order
     const cudaError_t e = cudaLaunchKernelEx(&cfg, pipe_kernel, a, map);
     if (e != cudaSuccess) {
       set_error(std::string("pipe_kernel: ") + cudaGetErrorString(e));

@@ -238,8 +238,9 @@ class MtbEngine:
             done = t.empty((max(P, 1), self.n), dtype=t.int32, device="cuda")
         ws = self.fused_workspace()
         sync = ws.get("sync")
-        if sync is None or sync.numel() < 17 * (n_img + 8):
-            sync = ws["sync"] = t.empty(17 * (n_img + 8), dtype=t.int32, device="cuda")
+        words = int(_lib.load().mtb_align_fused_sync_words(n_img, P, self.n))
+        if sync is None or sync.numel() < words:
+            sync = ws["sync"] = t.empty(words, dtype=t.int32, device="cuda")
         _lib.call("mtb_align_fused", _dev.ptr(rgb), 3 * self.width, 3 * self.width * self.height, self.width,
                   self.height, n_img, self.requested_levels, self.tol, pairs.ctypes.data, P, _dev.ptr(ws["gray"]),
                   _dev.ptr(pyr.hist_ws), _dev.ptr(pyr.medians), _dev.ptr(pyr.mtb), _dev.ptr(pyr.excl),

@@ -1,0 +1,153 @@
+// K3 microbenchmark: threshold+pack of a 24 MP pyramid's tile-major gray
+// (33 MB, L2-warm or cold) -> packed MTB/exclusion words.  Variants:
+//   A: one thread per 32-px word, 256-thread CTAs, grid-stride (occupancy-bound latency hiding)
+//   B: same, 2 words per thread
+// Reports time for L2-warm input (input rewritten just before) and cold.
+#include <cstdio>
+#include <cstdint>
+#include <cuda_runtime.h>
+
+__device__ __forceinline__ void th_word(const uint32_t (&g)[8], uint32_t med, uint32_t ym, uint32_t yml, uint32_t yt,
+                                        uint32_t ytl, uint32_t& mw, uint32_t& ew) {
+  constexpr uint32_t H = 0x80808080u, L7 = 0x7f7f7f7fu;
+  uint32_t m = 0, e = 0;
+#pragma unroll
+  for (int k = 0; k < 8; ++k) {
+    const uint32_t x = g[k];
+    const uint32_t s = (x & L7) + yml;
+    const uint32_t gm = ((x & ym) | (x & s) | (ym & s)) & H;
+    uint32_t d;
+    asm("vabsdiff4.u32.u32.u32 %0, %1, %2, %3;" : "=r"(d) : "r"(x), "r"(med), "r"(0u));
+    const uint32_t sd = (d & L7) + ytl;
+    const uint32_t ge = ((d & yt) | (d & sd) | (yt & sd)) & H;
+    m = (((gm * 0x00204081u) >> (28 - 4 * k)) & (0xfu << (4 * k))) | m;
+    e = (((ge * 0x00204081u) >> (28 - 4 * k)) & (0xfu << (4 * k))) | e;
+  }
+  mw = m;
+  ew = e;
+}
+
+// Pipe-balanced variant: per 4 px ALU = xl, gm (one LOP3, bit 7 of ym known), VABSDIFF4, dl, ge (one LOP3), 2 SHF;
+// FMA = 2 adds (IMAD.IADD), 2 gather multiplies, 2 IMAD accumulations.
+template <bool MED_LO>
+__device__ __forceinline__ void th_word2(const uint32_t (&g)[8], uint32_t med, uint32_t yml, uint32_t ytl,
+                                         uint32_t& mw, uint32_t& ew) {
+  constexpr uint32_t H = 0x80808080u, L7 = 0x7f7f7f7fu;
+  uint32_t m = 0, e = 0;
+#pragma unroll
+  for (int k = 0; k < 8; ++k) {
+    const uint32_t x = g[k];
+    uint32_t s;
+    asm("mad.lo.u32 %0, %1, 1, %2;" : "=r"(s) : "r"(x & L7), "r"(yml));        // FMA-pipe add
+    const uint32_t gm = MED_LO ? ((x | s) & H) : (x & s & H);
+    uint32_t d;
+    asm("vabsdiff4.u32.u32.u32 %0, %1, %2, %3;" : "=r"(d) : "r"(x), "r"(med), "r"(0u));
+    uint32_t sd;
+    asm("mad.lo.u32 %0, %1, 1, %2;" : "=r"(sd) : "r"(d & L7), "r"(ytl));
+    const uint32_t ge = (d | sd) & H;                                           // tol <= 127
+    uint32_t nm, ne;
+    asm("mad.lo.u32 %0, %1, %2, %3;" : "=r"(m) : "r"((gm * 0x00204081u) >> 28), "r"(1u << (4 * k)), "r"(m));
+    asm("mad.lo.u32 %0, %1, %2, %3;" : "=r"(e) : "r"((ge * 0x00204081u) >> 28), "r"(1u << (4 * k)), "r"(e));
+    (void)nm; (void)ne;
+  }
+  mw = m;
+  ew = e;
+}
+
+template <int WPT>
+__global__ void __launch_bounds__(256) k3b(const uint4* __restrict__ gray, int nwords, uint32_t* mtb, uint32_t* excl,
+                                          uint32_t medr) {
+  const uint32_t med = medr, ym = (255u - (medr & 0xff)) * 0x01010101u, yml = ym & 0x7f7f7f7fu;
+  const uint32_t yt = (255u - 4u) * 0x01010101u, ytl = yt & 0x7f7f7f7fu;
+  for (int w0 = (blockIdx.x * blockDim.x + threadIdx.x) * WPT; w0 < nwords; w0 += gridDim.x * blockDim.x * WPT) {
+    uint4 v[WPT][2];
+#pragma unroll
+    for (int q = 0; q < WPT; ++q) {
+      v[q][0] = __ldcs(gray + 2 * (w0 + q));
+      v[q][1] = __ldcs(gray + 2 * (w0 + q) + 1);
+    }
+#pragma unroll
+    for (int q = 0; q < WPT; ++q) {
+      const uint32_t g[8] = {v[q][0].x, v[q][0].y, v[q][0].z, v[q][0].w, v[q][1].x, v[q][1].y, v[q][1].z, v[q][1].w};
+      uint32_t m, e;
+      if ((medr & 0xff) <= 127) th_word2<true>(g, med, yml, ytl, m, e);
+      else th_word2<false>(g, med, yml, ytl, m, e);
+      mtb[w0 + q] = m;
+      excl[w0 + q] = e;
+    }
+  }
+}
+
+template <int WPT>
+__global__ void __launch_bounds__(256) k3a(const uint4* __restrict__ gray, int nwords, uint32_t* mtb, uint32_t* excl,
+                                          uint32_t medr, int discard) {
+  const uint32_t med = medr, ym = (255u - (medr & 0xff)) * 0x01010101u, yml = ym & 0x7f7f7f7fu;
+  const uint32_t yt = (255u - 4u) * 0x01010101u, ytl = yt & 0x7f7f7f7fu;
+  for (int w0 = (blockIdx.x * blockDim.x + threadIdx.x) * WPT; w0 < nwords; w0 += gridDim.x * blockDim.x * WPT) {
+    uint4 v[WPT][2];
+#pragma unroll
+    for (int q = 0; q < WPT; ++q) {
+      const int w = w0 + q * 0;  // contiguous per thread
+      v[q][0] = __ldcs(gray + 2 * (w0 + q));
+      v[q][1] = __ldcs(gray + 2 * (w0 + q) + 1);
+    }
+#pragma unroll
+    for (int q = 0; q < WPT; ++q) {
+      const uint32_t g[8] = {v[q][0].x, v[q][0].y, v[q][0].z, v[q][0].w, v[q][1].x, v[q][1].y, v[q][1].z, v[q][1].w};
+      uint32_t m, e;
+      th_word(g, med, ym, yml, yt, ytl, m, e);
+      mtb[w0 + q] = m;
+      excl[w0 + q] = e;
+    }
+    if (discard && (threadIdx.x & 3) == 0 && WPT == 1)
+      asm volatile("discard.global.L2 [%0], 128;" ::"l"(gray + 2 * w0) : "memory");
+  }
+}
+__global__ void fill(uint4* p, size_t n) {
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x)
+    p[i] = make_uint4(i * 2654435761u, i * 40503u, i ^ 0x5bd1e995u, i * 97u);
+}
+__global__ void flush(const uint4* p, size_t n, unsigned* sink) {
+  unsigned a = 0;
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x) a ^= __ldcs(p + i).x;
+  if (a == 0x1234567) *sink = a;
+}
+int main() {
+  const int nwords = (24000000 + 8000000) / 32;   // 32 MP of gray -> words
+  uint4* gray; uint32_t *m, *e; uint4* big; unsigned* sink;
+  cudaMalloc(&gray, (size_t)nwords * 32); cudaMalloc(&m, nwords * 4); cudaMalloc(&e, nwords * 4);
+  cudaMalloc(&big, 512u << 20); cudaMalloc(&sink, 4);
+  cudaEvent_t a, b; cudaEventCreate(&a); cudaEventCreate(&b);
+  for (int variant = 0; variant < 2; ++variant) {
+    float best = 1e9;
+    for (int rep = 0; rep < 5; ++rep) {
+      fill<<<1184, 256>>>(gray, (size_t)nwords * 2);
+      cudaEventRecord(a);
+      if (variant == 0) k3b<1><<<148 * 8, 256>>>(gray, nwords, m, e, 0x80808080u);
+      else k3b<2><<<148 * 8, 256>>>(gray, nwords, m, e, 0x80808080u);
+      cudaEventRecord(b); cudaEventSynchronize(b);
+      float ms; cudaEventElapsedTime(&ms, a, b); if (ms < best) best = ms;
+    }
+    printf("balanced k3b wpt %d: %.1f us\n", variant + 1, best * 1e3);
+  }
+  for (int variant = 0; variant < 6; ++variant) {
+    const int wpt = variant % 3 == 0 ? 1 : (variant % 3 == 1 ? 2 : 4);
+    const bool warm = variant < 3;
+    float best = 1e9;
+    for (int rep = 0; rep < 5; ++rep) {
+      flush<<<1184, 256>>>(big, (512u << 20) / 16, sink);
+      fill<<<1184, 256>>>(gray, (size_t)nwords * 2);
+      if (!warm) flush<<<1184, 256>>>(big, (512u << 20) / 16, sink);
+      cudaEventRecord(a);
+      const int blocks = 148 * 8;
+      if (wpt == 1) k3a<1><<<blocks, 256>>>(gray, nwords, m, e, 0x80808080u, 0);
+      else if (wpt == 2) k3a<2><<<blocks, 256>>>(gray, nwords, m, e, 0x80808080u, 0);
+      else k3a<4><<<blocks, 256>>>(gray, nwords, m, e, 0x80808080u, 0);
+      cudaEventRecord(b); cudaEventSynchronize(b);
+      float ms; cudaEventElapsedTime(&ms, a, b); if (ms < best) best = ms;
+    }
+    printf("%s words/thread %d: %.1f us (%.0f GB/s gray)\n", warm ? "L2-warm" : "cold   ", wpt, best * 1e3,
+           (double)nwords * 32 / (best * 1e-3) / 1e9);
+  }
+  return 0;
+}
