@@ -86,10 +86,16 @@ struct ThConst {
 // Warp roles: warps 0..7 = two K1 groups streaming image j (never wait on
 // earlier launches: the gray ring has 3 slots), warps 8..15 = the aux warps
 // (K3 + search) which wait for launch j-1.
-constexpr int kPK1Groups = 2;
+#ifndef PIPE_K1_GROUPS
+#define PIPE_K1_GROUPS 3
+#endif
+#ifndef PIPE_STAGES
+#define PIPE_STAGES 2
+#endif
+constexpr int kPK1Groups = PIPE_K1_GROUPS;
 constexpr int kPK1Warps = 4 * kPK1Groups;
 constexpr int kPAuxWarps = kPipeWarps - kPK1Warps;
-constexpr int kPStages = 3;
+constexpr int kPStages = PIPE_STAGES;
 constexpr int kPGraySlots = 3;
 constexpr int kAuxPhases = 7;     // aux task phases: K3 levels 0..3, levels 4..5, padding, search
 
@@ -103,7 +109,7 @@ struct SearchStage {
 struct PipeSmem {
   uint32_t hist[6][256];                                  // 1 KB-aligned levels (see k1_tile.cuh)
   uint8_t rgb[kPK1Groups][kPStages][kK1TileBytes];
-  uint8_t abuf[kPAuxWarps][2][4096];                      // aux warps: K3 double buffer / search staging
+  uint8_t abuf[kPAuxWarps > 0 ? kPAuxWarps : 1][2][4096];                      // aux warps: K3 double buffer / search staging
   uint8_t l3[kPK1Groups][2][4][32];
   unsigned long long full[kPK1Groups][kPStages];
   int tile_of[kPK1Groups][kPStages];                      // tile in each ring stage (-1: no more)
@@ -112,6 +118,7 @@ struct PipeSmem {
   int last;
   int next;                                               // aux task queue head
   int plo[kAuxPhases], pcnt[kAuxPhases];                  // this CTA's slice of each aux phase
+  int sleft;                                              // this CTA's search tiles not yet done
   unsigned scnt[kPipeMaxItems][9];                        // per-item partial search counts
 };
 constexpr int kPipeSmemBytes = (int)sizeof(PipeSmem) + 1024;
@@ -181,6 +188,12 @@ template <bool MED_LO, bool TOL_LO>
 __device__ __forceinline__ void th_word_t(const uint32_t (&g)[8], const ThConst& c, uint32_t yt, uint32_t ytl,
                                           int valid, uint32_t& mw, uint32_t& ew) {
   constexpr uint32_t H = 0x80808080u, L7 = 0x7f7f7f7fu;
+  // Gather: umulhi(flags, magic << 4) puts the 4 byte flags (bits 7,15,23,31)
+  // in bits 0..3 of the high word (other terms land below bit 32 or at >= bit
+  // 40); a funnel shift (nib:acc) >> 4 pushes them in from the top and drops
+  // the garbage, so after 8 words word k's flags sit at bits 4k..4k+3.  One
+  // FMA-pipe and one ALU-pipe op per word and map.
+  constexpr uint32_t M4 = 0x00204081u << 4;
   uint32_t m = 0, e = 0;
 #pragma unroll
   for (int k = 0; k < 8; ++k) {
@@ -191,9 +204,8 @@ __device__ __forceinline__ void th_word_t(const uint32_t (&g)[8], const ThConst&
     asm("vabsdiff4.u32.u32.u32 %0, %1, %2, %3;" : "=r"(d) : "r"(x), "r"(c.med), "r"(0u));
     const uint32_t sd = (d & L7) + ytl;
     const uint32_t ge = TOL_LO ? ((d | sd) & H) : (((d & yt) | (d & sd) | (yt & sd)) & H);   // |x - med| > tol
-    // flags at bits 7,15,23,31 -> bits 28..31 of the product -> bits 4k..4k+3
-    m = (((gm * 0x00204081u) >> (28 - 4 * k)) & (0xfu << (4 * k))) | m;
-    e = (((ge * 0x00204081u) >> (28 - 4 * k)) & (0xfu << (4 * k))) | e;
+    m = __funnelshift_r(m, __umulhi(gm, M4), 4);
+    e = __funnelshift_r(e, __umulhi(ge, M4), 4);
   }
   const uint32_t keep = valid >= 32 ? 0xffffffffu : (valid <= 0 ? 0u : ((1u << valid) - 1u));
   mw = m & keep;
@@ -661,7 +673,7 @@ __device__ __forceinline__ void pipe_search_flush(const PipeArgs& a, const PipeI
 // wait, the K1 warps once their tiles are done — so the CTA's K1 and aux
 // work finish together.
 static_assert(sizeof(SearchStage) <= 8192, "search staging fits a warp's 2 x 4 KB K3 buffers");
-static_assert(kPStages * kK1TileBytes >= 4 * 16384, "K1 warps stage in their group ring");
+static_assert(kPStages * kK1TileBytes >= 4 * 12288, "K1 warps stage in their group ring");
 
 struct AuxCtx {
   const uint8_t* slot;
@@ -745,12 +757,13 @@ __device__ __forceinline__ void aux_run(const PipeArgs& a, PipeSmem& S, const Au
 // equal static slices stay balanced).  Task order within the CTA: K3 levels
 // 0..3 (4 units each), levels 4..5, padding, search tiles — or search first
 // (a.search_first).
-__device__ __forceinline__ int aux_phase_of(const PipeArgs& a, int q) {
-  return a.search_first ? (q == 0 ? 6 : q - 1) : q;
-}
+// Queue order q -> phase: search tiles first (the longest tasks; their CTA
+// partial counts are flushed as soon as the CTA's last tile is done, so the
+// next launch's level can start early), then K3 levels 0..3, 4..5, padding.
+__device__ __forceinline__ int aux_phase_of(const PipeArgs& a, int q) { return q == 0 ? 6 : q - 1; }
 
 __device__ __forceinline__ void aux_drain(const PipeArgs& a, PipeSmem& S, const AuxCtx& x) {
-  int lo[kAuxPhases], cnt[kAuxPhases];   // this CTA's slices (computed once per CTA, aux prologue)
+  int lo[kAuxPhases], cnt[kAuxPhases];   // this CTA's slices in queue order (aux prologue)
 #pragma unroll
   for (int q = 0; q < kAuxPhases; ++q) {
     lo[q] = S.plo[q];
@@ -772,6 +785,7 @@ __device__ __forceinline__ void aux_drain(const PipeArgs& a, PipeSmem& S, const 
     int q = 0;
     while (q < kAuxPhases && t >= cnt[q]) t -= cnt[q++];
     const int p = q < kAuxPhases ? aux_phase_of(a, q) : -1;
+    const int r = q < kAuxPhases ? lo[q] + t : 0;
     if (p >= 0 && x.tracer && x.lane == 0 && a.trace) {
       unsigned long long* slot = a.trace + ((int64_t)a.j * gridDim.x + blockIdx.x) * 16 + 8 + p;
       if (*slot == 0) {
@@ -780,28 +794,68 @@ __device__ __forceinline__ void aux_drain(const PipeArgs& a, PipeSmem& S, const 
         *slot = tt;
       }
     }
-    if (p >= 0 && p < 4) {
-      k3_bulk_issue(a, x.slot, p, lo[q] + t, x.lane, x.kbuf + nb * 4096, &x.kbar[nb]);
-      if (pend_k >= 0) {
-        k3_bulk_finish(a, x.slot, x.mtb, x.excl, S.th, x.yt, x.ytl, pend_k, pend_r, x.lane, x.kbuf + pend_b * 4096,
-                       &x.kbar[pend_b], par[pend_b]);
-        par[pend_b] ^= 1u;
-      }
-      pend_k = p;
-      pend_r = lo[q] + t;
-      pend_b = nb;
-      nb ^= 1;
-      continue;
-    }
-    if (pend_k >= 0) {
+    const bool k3 = p >= 0 && p < 4;
+    if (k3) k3_bulk_issue(a, x.slot, p, r, x.lane, x.kbuf + nb * 4096, &x.kbar[nb]);
+    if (pend_k >= 0) {   // the one call site of the K3 compute
       k3_bulk_finish(a, x.slot, x.mtb, x.excl, S.th, x.yt, x.ytl, pend_k, pend_r, x.lane, x.kbuf + pend_b * 4096,
                      &x.kbar[pend_b], par[pend_b]);
       par[pend_b] ^= 1u;
       pend_k = -1;
     }
+    if (k3) {
+      pend_k = p;
+      pend_r = r;
+      pend_b = nb;
+      nb ^= 1;
+      continue;
+    }
     if (p < 0) return;
-    aux_run(a, S, x, p, lo[q] + t);
+    aux_run(a, S, x, p, r);
+    if (p == 6) {
+      // last search tile of this CTA: publish its partial counts
+      __syncwarp();
+      int left = 0;
+      if (x.lane == 0) {
+        __threadfence_block();
+        left = atomicSub(&S.sleft, 1) - 1;
+      }
+      left = __shfl_sync(0xffffffffu, left, 0);
+      if (left == 0) {
+        __threadfence_block();
+        for (int i = x.lane; i < a.n_items; i += 32) pipe_search_flush(a, a.items[i], S.scnt[i]);
+      }
+    }
   }
+}
+
+// Before any aux task of launch j: image th_img's medians published
+// (spin), threshold constants, the CTA's task slices, queue and search
+// counters reset.  Run by `n` threads (at = 0..n-1) synchronised on `bar`.
+__device__ __forceinline__ void aux_prologue(const PipeArgs& a, PipeSmem& S, int at, int n, int bar) {
+  if (at == 0 && a.th_img >= 0) spin_geq(a.med_ready + a.th_img, 1u);   // image th_img's K1 published
+  named_bar(bar, n);
+  if (a.th_img >= 0 && at < a.n) {
+    const int med = __ldcg(a.medians + a.th_img * a.n + at);
+    ThConst c;
+    c.med = (uint32_t)med * 0x01010101u;
+    c.ym = (uint32_t)(255 - med) * 0x01010101u;
+    c.yml = c.ym & 0x7f7f7f7fu;
+    c.med_lo = med <= 127;
+    S.th[at] = c;
+  }
+  if (at == 0) S.next = 0;
+  if (at < kAuxPhases) {
+    const int G = gridDim.x, c = blockIdx.x;
+    const int T = aux_phase_tasks(a, aux_phase_of(a, at));
+    S.plo[at] = (int)((int64_t)c * T / G);
+    S.pcnt[at] = (int)((int64_t)(c + 1) * T / G) - S.plo[at];
+  }
+  for (int i = at; i < a.n_items * 9; i += n) (&S.scnt[0][0])[i] = 0;
+  named_bar(bar, n);
+  if (at == 0) S.sleft = S.pcnt[0];   // queue phase 0 = search tiles
+  // a CTA without search tiles still counts towards every item's completion
+  if (S.pcnt[0] == 0 && at < a.n_items) pipe_search_flush(a, a.items[at], S.scnt[at]);
+  named_bar(bar, n);
 }
 
 __global__ void __launch_bounds__(kK1Threads, 1) pipe_kernel(const __grid_constant__ PipeArgs a,
@@ -831,8 +885,8 @@ __global__ void __launch_bounds__(kK1Threads, 1) pipe_kernel(const __grid_consta
     const int kt = tid;               // 0..255 among the K1 threads
     const uint32_t hb = smem_addr(&S.hist[0][0]);
     stamp(0);
-    if (a.k1_img >= 0 && a.probe != 1) {
-      const int tiles_img = a.g.tiles_x * a.g.tiles_y;
+    if (a.k1_img >= 0) {
+      const int tiles_img = a.probe == 1 ? 0 : a.g.tiles_x * a.g.tiles_y;   // probe 1: no tiles, still publish
       uint32_t* ctr = a.ctr + a.j;   // K1 tile counter of this launch
       uint64_t pol_first;
       asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol_first));
@@ -933,36 +987,14 @@ __global__ void __launch_bounds__(kK1Threads, 1) pipe_kernel(const __grid_consta
       stamp(2);
     }
     // Join the aux work.
-    asm volatile("bar.sync 9, %0;" ::"r"(kK1Threads) : "memory");   // S.th / S.next ready
+    if constexpr (kPAuxWarps > 0) {
+      asm volatile("bar.sync 9, %0;" ::"r"(kK1Threads) : "memory");   // S.th / S.next ready
+    } else {
+      aux_prologue(a, S, tid, kK1Threads, 9);
+    }
   } else {
     // ======================= aux warps: K3 + search ==========================
-    const int at = tid - 32 * kPK1Warps;    // 0..255
-    if (at == 0 && a.th_img >= 0) spin_geq(a.med_ready + a.th_img, 1u);   // image th_img's K1 published
-    named_bar(6, 32 * kPAuxWarps);
-    stamp(4);
-    if (a.trace && at == 0) {
-      unsigned smid;
-      asm volatile("mov.u32 %0, %smid;" : "=r"(smid));
-      a.trace[((int64_t)a.j * gridDim.x + blockIdx.x) * 16 + 6] = smid;
-    }
-    if (a.th_img >= 0 && at < a.n) {
-      const int med = __ldcg(a.medians + a.th_img * a.n + at);
-      ThConst c;
-      c.med = (uint32_t)med * 0x01010101u;
-      c.ym = (uint32_t)(255 - med) * 0x01010101u;
-      c.yml = c.ym & 0x7f7f7f7fu;
-      c.med_lo = med <= 127;
-      S.th[at] = c;
-    }
-    if (at == 0) S.next = 0;
-    if (at < kAuxPhases) {
-      const int G = gridDim.x, c = blockIdx.x;
-      const int T = aux_phase_tasks(a, aux_phase_of(a, at));
-      S.plo[at] = (int)((int64_t)c * T / G);
-      S.pcnt[at] = (int)((int64_t)(c + 1) * T / G) - S.plo[at];
-    }
-    for (int i = at; i < a.n_items * 9; i += 32 * kPAuxWarps) (&S.scnt[0][0])[i] = 0;
-    named_bar(6, 32 * kPAuxWarps);
+    aux_prologue(a, S, tid - 32 * kPK1Warps, 32 * kPAuxWarps, 6);
     asm volatile("bar.arrive 9, %0;" ::"r"(kK1Threads) : "memory");
   }
 
@@ -977,7 +1009,7 @@ __global__ void __launch_bounds__(kK1Threads, 1) pipe_kernel(const __grid_consta
   // K1 warps stage in their group's ring (all its TMA copies have landed,
   // 16 KB per warp); aux warps in their own 8 KB
   ax.kbuf = warp < kPK1Warps
-                ? &S.rgb[0][0][0] + (size_t)(warp >> 2) * (kPStages * kK1TileBytes) + (warp & 3) * 16384
+                ? &S.rgb[0][0][0] + (size_t)(warp >> 2) * (kPStages * kK1TileBytes) + (warp & 3) * 12288
                 : &S.abuf[warp - kPK1Warps][0][0];
   ax.kbar = S.kbar[warp];
   ax.stage = reinterpret_cast<SearchStage*>(ax.kbuf);
@@ -989,8 +1021,6 @@ __global__ void __launch_bounds__(kK1Threads, 1) pipe_kernel(const __grid_consta
     __threadfence();
     atomicAdd(a.k3_done + a.th_img, 1u);
   }
-  const int ft = tid - 32 * kPK1Warps;
-  if (ft >= 0 && ft < a.n_items) pipe_search_flush(a, a.items[ft], S.scnt[ft]);
 }
 
 bool k1_rgb_supported(int w, int64_t rgb_pitch, int64_t rgb_img_stride, const void* rgb);

@@ -54,6 +54,54 @@ __device__ __forceinline__ void th_word2(const uint32_t (&g)[8], uint32_t med, u
   ew = e;
 }
 
+// Funnel-shift gather: nib = umulhi(flags, magic << 4) (FMA pipe) holds the 4
+// flags in bits 0..3 (garbage only at bits >= 8); acc = (nib:acc) >> 4 (one SHF)
+// pushes them in from the top, garbage shifted out.
+template <bool MED_LO>
+__device__ __forceinline__ void th_word3(const uint32_t (&g)[8], uint32_t med, uint32_t yml, uint32_t ytl,
+                                         uint32_t& mw, uint32_t& ew) {
+  constexpr uint32_t H = 0x80808080u, L7 = 0x7f7f7f7fu, M4 = 0x00204081u << 4;
+  uint32_t m = 0, e = 0;
+#pragma unroll
+  for (int k = 0; k < 8; ++k) {
+    const uint32_t x = g[k];
+    const uint32_t s = (x & L7) + yml;
+    const uint32_t gm = MED_LO ? ((x | s) & H) : (x & s & H);
+    uint32_t d;
+    asm("vabsdiff4.u32.u32.u32 %0, %1, %2, %3;" : "=r"(d) : "r"(x), "r"(med), "r"(0u));
+    const uint32_t sd = (d & L7) + ytl;
+    const uint32_t ge = (d | sd) & H;
+    m = __funnelshift_r(m, __umulhi(gm, M4), 4);
+    e = __funnelshift_r(e, __umulhi(ge, M4), 4);
+  }
+  mw = m;
+  ew = e;
+}
+
+template <int WPT>
+__global__ void __launch_bounds__(256) k3c(const uint4* __restrict__ gray, int nwords, uint32_t* mtb, uint32_t* excl,
+                                          uint32_t medr) {
+  const uint32_t med = medr, ym = (255u - (medr & 0xff)) * 0x01010101u, yml = ym & 0x7f7f7f7fu;
+  const uint32_t yt = (255u - 4u) * 0x01010101u, ytl = yt & 0x7f7f7f7fu;
+  for (int w0 = (blockIdx.x * blockDim.x + threadIdx.x) * WPT; w0 < nwords; w0 += gridDim.x * blockDim.x * WPT) {
+    uint4 v[WPT][2];
+#pragma unroll
+    for (int q = 0; q < WPT; ++q) {
+      v[q][0] = __ldcs(gray + 2 * (w0 + q));
+      v[q][1] = __ldcs(gray + 2 * (w0 + q) + 1);
+    }
+#pragma unroll
+    for (int q = 0; q < WPT; ++q) {
+      const uint32_t g[8] = {v[q][0].x, v[q][0].y, v[q][0].z, v[q][0].w, v[q][1].x, v[q][1].y, v[q][1].z, v[q][1].w};
+      uint32_t m, e;
+      if ((medr & 0xff) <= 127) th_word3<true>(g, med, yml, ytl, m, e);
+      else th_word3<false>(g, med, yml, ytl, m, e);
+      mtb[w0 + q] = m;
+      excl[w0 + q] = e;
+    }
+  }
+}
+
 template <int WPT>
 __global__ void __launch_bounds__(256) k3b(const uint4* __restrict__ gray, int nwords, uint32_t* mtb, uint32_t* excl,
                                           uint32_t medr) {
@@ -118,6 +166,31 @@ int main() {
   cudaMalloc(&gray, (size_t)nwords * 32); cudaMalloc(&m, nwords * 4); cudaMalloc(&e, nwords * 4);
   cudaMalloc(&big, 512u << 20); cudaMalloc(&sink, 4);
   cudaEvent_t a, b; cudaEventCreate(&a); cudaEventCreate(&b);
+  {
+    // correctness: k3c == k3a on random data for medians 40 and 200
+    uint32_t *m2, *e2; cudaMalloc(&m2, nwords * 4); cudaMalloc(&e2, nwords * 4);
+    for (uint32_t medv : {40u, 200u}) {
+      fill<<<1184, 256>>>(gray, (size_t)nwords * 2);
+      k3a<1><<<148 * 8, 256>>>(gray, nwords, m, e, medv * 0x01010101u, 0);
+      k3c<1><<<148 * 8, 256>>>(gray, nwords, m2, e2, medv * 0x01010101u);
+      cudaDeviceSynchronize();
+      uint32_t* h1 = (uint32_t*)malloc(nwords * 4); uint32_t* h2 = (uint32_t*)malloc(nwords * 4);
+      cudaMemcpy(h1, m, nwords * 4, cudaMemcpyDeviceToHost); cudaMemcpy(h2, m2, nwords * 4, cudaMemcpyDeviceToHost);
+      int bad = 0; for (int i = 0; i < nwords; ++i) bad += h1[i] != h2[i];
+      cudaMemcpy(h1, e, nwords * 4, cudaMemcpyDeviceToHost); cudaMemcpy(h2, e2, nwords * 4, cudaMemcpyDeviceToHost);
+      for (int i = 0; i < nwords; ++i) bad += h1[i] != h2[i];
+      printf("k3c vs k3a med %u: %d mismatches\n", medv, bad);
+    }
+    float best = 1e9;
+    for (int rep = 0; rep < 5; ++rep) {
+      fill<<<1184, 256>>>(gray, (size_t)nwords * 2);
+      cudaEventRecord(a);
+      k3c<1><<<148 * 8, 256>>>(gray, nwords, m, e, 0x80808080u);
+      cudaEventRecord(b); cudaEventSynchronize(b);
+      float ms; cudaEventElapsedTime(&ms, a, b); if (ms < best) best = ms;
+    }
+    printf("funnel-gather k3c: %.1f us\n", best * 1e3);
+  }
   for (int variant = 0; variant < 2; ++variant) {
     float best = 1e9;
     for (int rep = 0; rep < 5; ++rep) {
