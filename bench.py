@@ -50,7 +50,7 @@ def parse():
     ap.add_argument("--height", type=int, default=4000)
     ap.add_argument("--levels", type=int, default=6)
     ap.add_argument("--tol", type=int, default=4)
-    ap.add_argument("--mode", choices=("fused", "staged"), default="staged",
+    ap.add_argument("--mode", choices=("fused", "staged"), default="fused",
                     help="fused: one pipelined launch per image (csrc/pipe.cu); staged: K1 / K3 / K4 kernels")
     ap.add_argument("--chunk", type=int, default=0,
                     help="images per preprocess round (K1 launches then threshold); 0 = whole batch")
@@ -375,10 +375,15 @@ def run_e2e(args, torch, eng, batch, pyr, table, acc, errs, done, P):
     stream = torch.cuda.current_stream()
     n_img = 2 * P
 
+    fused = args.mode == "fused"
+
     def step():
         dev_in.copy_(host, non_blocking=True)
-        eng.preprocess(dev_in, pyr, count=False)
-        eng.search_table(table_in, P, acc, errs, done, count=False)
+        if fused:
+            eng.align_fused(dev_in, pairs, pyr, acc, errs, done, count=False)
+        else:
+            eng.preprocess(dev_in, pyr, count=False)
+            eng.search_table(table_in, P, acc, errs, done, count=False)
         out_host.copy_(acc[:, 0], non_blocking=True)
 
     pairs = [(2 * p, 2 * p + 1) for p in range(P)]
@@ -395,7 +400,8 @@ def run_e2e(args, torch, eng, batch, pyr, table, acc, errs, done, P):
     dt = s.elapsed_time(e) / 1e3
     return {"value": round(P * args.e2e_steps / dt, 2), "unit": UNIT,
             "h2d_bytes_per_step": int(host.numel()), "d2h_bytes_per_step": int(out_host.numel() * 4),
-            "api": "MtbEngine.preprocess + search_table on an H2D-copied pinned batch"}
+            "api": ("MtbEngine.align_fused" if args.mode == "fused" else "MtbEngine.preprocess + search_table")
+                   + " on an H2D-copied pinned batch"}
 
 
 def main():

@@ -604,7 +604,7 @@ __device__ __forceinline__ void pipe_search_tile(const PipeArgs& a, const PipeIt
   uint32_t b0[3], e0[3], b1[3], e1[3];
   shifted(0, b0, e0);
   shifted(1, b1, e1);
-#pragma unroll
+#pragma unroll 2
   for (int rr = 0; rr < 8; ++rr) {
     uint32_t b2[3], e2[3];
     shifted(rr + 2, b2, e2);

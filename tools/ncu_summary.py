@@ -72,7 +72,14 @@ def main():
     per_kernel = collections.OrderedDict()
     for d in fm:
         per_kernel.setdefault(d["kernel"], []).append(d)
+    # merge with an existing summary: kernels captured earlier keep their entries
+    path = os.path.join(a.out, "ncu_summary.json")
     summary = {"source": os.path.basename(a.full), "tag": a.tag, "kernels": {}, "detail": {}}
+    if os.path.exists(path):
+        with open(path) as f:
+            old = json.load(f)
+        summary["kernels"].update(old.get("kernels", {}))
+        summary["detail"].update(old.get("detail", {}))
     for k, ds in per_kernel.items():
         traffic = [d["dram__bytes_read.sum"] + d["dram__bytes_write.sum"] for d in ds]
         summary["kernels"][k] = round(sum(traffic) / len(traffic))
