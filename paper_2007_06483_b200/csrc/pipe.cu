@@ -33,7 +33,15 @@ namespace mtb {
 
 constexpr int kPipeMaxLevels = 6;
 constexpr int kPipeMaxItems = 96;
-constexpr int kPipeWarps = kK1Threads / 32;   // 16
+#ifndef PIPE_THREADS
+#define PIPE_THREADS 512
+#endif
+constexpr int kPipeThreads = PIPE_THREADS;     // 12 K1 warps + 4 aux warps
+constexpr int kPipeWarps = kPipeThreads / 32;
+constexpr int kK3Units = 4;                     // K3 task = 4 x 32 bitmap words = 4 KB of gray
+constexpr int kK3Words = 32 * kK3Units;
+constexpr int kK3Bytes = 32 * kK3Words;
+constexpr int kSRows = 8;                       // search tile: 8 output rows x 32 words
 
 struct PipeItem {
   int pair;      // index into acc/errs/done
@@ -102,14 +110,14 @@ constexpr int kAuxPhases = 7;     // aux task phases: K3 levels 0..3, levels 4..
 // Per-aux-warp staging of one search warp-tile: 8 output rows x 32 words of
 // the reference maps, 10 source rows x 35 words of the target maps.
 struct SearchStage {
-  uint32_t a[8][32], ea[8][32];
-  uint32_t b[10][36], eb[10][36];
+  uint32_t a[kSRows][32], ea[kSRows][32];
+  uint32_t b[kSRows + 2][36], eb[kSRows + 2][36];
 };
 
 struct PipeSmem {
   uint32_t hist[6][256];                                  // 1 KB-aligned levels (see k1_tile.cuh)
   uint8_t rgb[kPK1Groups][kPStages][kK1TileBytes];
-  uint8_t abuf[kPAuxWarps > 0 ? kPAuxWarps : 1][2][4096];                      // aux warps: K3 double buffer / search staging
+  uint8_t abuf[kPAuxWarps > 0 ? kPAuxWarps : 1][2][kK3Bytes];                  // aux warps: K3 double buffer / search staging
   uint8_t l3[kPK1Groups][2][4][32];
   unsigned long long full[kPK1Groups][kPStages];
   int tile_of[kPK1Groups][kPStages];                      // tile in each ring stage (-1: no more)
@@ -369,13 +377,13 @@ __device__ __forceinline__ void k3_bulk_issue(const PipeArgs& a, const uint8_t* 
                                               uint8_t* buf, unsigned long long* bar) {
   const int lwpt = 8 - 2 * K;
   const int wpt = 1 << lwpt;
-  const int pw = wpt < 128 ? wpt : 128;          // words per piece
-  const int npieces = 128 / pw;
+  const int pw = wpt < kK3Words ? wpt : kK3Words;   // words per piece
+  const int npieces = kK3Words / pw;
   const int ntiles = a.g.tiles_x * a.g.tiles_y;
-  const int f0 = 128 * r;
+  const int f0 = kK3Words * r;
   // bytes that exist (pieces of tiles past the end are not copied)
-  const int tiles_needed = ((f0 + 127) >> lwpt) - (f0 >> lwpt) + 1;
-  int bytes = 4096;
+  const int tiles_needed = ((f0 + kK3Words - 1) >> lwpt) - (f0 >> lwpt) + 1;
+  int bytes = kK3Bytes;
   if ((f0 >> lwpt) + tiles_needed > ntiles) {
     const int last_f = ntiles << lwpt;                  // words that exist at this level
     bytes = (last_f - f0) * 32;
@@ -405,9 +413,9 @@ __device__ __forceinline__ void k3_bulk_units(const PipeArgs& a, uint32_t* mtb, 
   const int ntiles = a.g.tiles_x * a.g.tiles_y;
   const int nw = a.nw32[K], lh = a.g.lh[K], lw = a.g.lw[K];
   const int boff = (int)a.bit_off32[K];
-  const int f0 = 128 * r;
+  const int f0 = kK3Words * r;
 #pragma unroll
-  for (int i = 0; i < 4; ++i) {
+  for (int i = 0; i < kK3Units; ++i) {
     const int w = i * 32 + lane;
     const int f = f0 + w;
     const int t = f >> lwpt;
@@ -435,8 +443,8 @@ __device__ __forceinline__ void k3_bulk_finish(const PipeArgs& a, const uint8_t*
   const ThConst c = th[K];
   if (a.tol > 127) {
     // rare: generic majority for the exclusion compare
-    const int f0 = 128 * r;
-    for (int i = 0; i < 4; ++i) {
+    const int f0 = kK3Words * r;
+    for (int i = 0; i < kK3Units; ++i) {
       const int w = i * 32 + lane, f = f0 + w;
       const int lwpr = 3 - K, lwpt = 8 - 2 * K;
       const int t = f >> lwpt, rem = f & ((1 << lwpt) - 1);
@@ -461,9 +469,9 @@ __device__ __forceinline__ void k3_bulk_finish(const PipeArgs& a, const uint8_t*
   }
   const int lwpt = 8 - 2 * K, wpt = 1 << lwpt;
   const int ntiles = a.g.tiles_x * a.g.tiles_y;
-  // line `lane` of the task's 4 KB: drop it from L2 without write-back
-  {
-    const int f = 128 * r + 4 * lane;
+  // line `lane` of the task's gray: drop it from L2 without write-back
+  if (lane < kK3Bytes / 128) {
+    const int f = kK3Words * r + 4 * lane;
     const int t = f >> lwpt;
     if (t < ntiles)
       asm volatile("discard.global.L2 [%0], 128;" ::"l"(slot + (int64_t)t * kTileGrayBytes + tm_off(K) +
@@ -517,7 +525,7 @@ __device__ __forceinline__ void pipe_search_tile(const PipeArgs& a, const PipeIt
   const int nw = a.nw32[k];
   const int cpr = (nw + 31) >> 5;
   const int rb = tile / cpr, cb = tile - rb * cpr;
-  const int y0 = rb * 8;
+  const int y0 = rb * kSRows;
   const int j0 = cb * 32;
   const int n = a.n;
   if (lane == 0) {
@@ -545,7 +553,7 @@ __device__ __forceinline__ void pipe_search_tile(const PipeArgs& a, const PipeIt
   {
     const int j = j0 + lane;
 #pragma unroll
-    for (int r = 0; r < 8; ++r) {
+    for (int r = 0; r < kSRows; ++r) {
       const int y = y0 + r;
       const bool ok = y < h && j < nw;
       const int64_t o = ok ? (int64_t)y * nw + j : 0;
@@ -554,7 +562,7 @@ __device__ __forceinline__ void pipe_search_tile(const PipeArgs& a, const PipeIt
     }
     const int sy0 = y0 - by - 1;
 #pragma unroll
-    for (int r = 0; r < 10; ++r) {
+    for (int r = 0; r < kSRows + 2; ++r) {
       const int sy = sy0 + r;
       const bool rok = sy >= 0 && sy < h;
 #pragma unroll
@@ -605,7 +613,7 @@ __device__ __forceinline__ void pipe_search_tile(const PipeArgs& a, const PipeIt
   shifted(0, b0, e0);
   shifted(1, b1, e1);
 #pragma unroll 2
-  for (int rr = 0; rr < 8; ++rr) {
+  for (int rr = 0; rr < kSRows; ++rr) {
     uint32_t b2[3], e2[3];
     shifted(rr + 2, b2, e2);
     const uint32_t av = sm.a[rr][lane], ev = sm.ea[rr][lane];
@@ -672,7 +680,7 @@ __device__ __forceinline__ void pipe_search_flush(const PipeArgs& a, const PipeI
 // shared-memory counter — the aux warps right after the grid dependency
 // wait, the K1 warps once their tiles are done — so the CTA's K1 and aux
 // work finish together.
-static_assert(sizeof(SearchStage) <= 8192, "search staging fits a warp's 2 x 4 KB K3 buffers");
+static_assert(sizeof(SearchStage) <= 2 * kK3Bytes, "search staging fits a warp's two K3 buffers");
 static_assert(kPStages * kK1TileBytes >= 4 * 12288, "K1 warps stage in their group ring");
 
 struct AuxCtx {
@@ -693,10 +701,10 @@ __device__ __forceinline__ void named_bar(int id, int n) { asm volatile("bar.syn
 __device__ __forceinline__ int aux_phase_tasks(const PipeArgs& a, int p) {
   const bool th = a.th_img >= 0;
   switch (p) {
-    case 0: return th ? (th_level_units<0>(a) + 3) / 4 : 0;
-    case 1: return th && a.n > 1 ? (th_level_units<1>(a) + 3) / 4 : 0;
-    case 2: return th && a.n > 2 ? (th_level_units<2>(a) + 3) / 4 : 0;
-    case 3: return th && a.n > 3 ? (th_level_units<3>(a) + 3) / 4 : 0;
+    case 0: return th ? (th_level_units<0>(a) + kK3Units - 1) / kK3Units : 0;
+    case 1: return th && a.n > 1 ? (th_level_units<1>(a) + kK3Units - 1) / kK3Units : 0;
+    case 2: return th && a.n > 2 ? (th_level_units<2>(a) + kK3Units - 1) / kK3Units : 0;
+    case 3: return th && a.n > 3 ? (th_level_units<3>(a) + kK3Units - 1) / kK3Units : 0;
     case 4: return th ? a.th_units0[a.n] - a.th_units0[a.n < 4 ? a.n : 4] : 0;
     case 5: return th ? (a.th_pad_words + 31) / 32 : 0;
     default: return a.search_tiles;   // 6
@@ -795,9 +803,9 @@ __device__ __forceinline__ void aux_drain(const PipeArgs& a, PipeSmem& S, const 
       }
     }
     const bool k3 = p >= 0 && p < 4;
-    if (k3) k3_bulk_issue(a, x.slot, p, r, x.lane, x.kbuf + nb * 4096, &x.kbar[nb]);
+    if (k3) k3_bulk_issue(a, x.slot, p, r, x.lane, x.kbuf + nb * kK3Bytes, &x.kbar[nb]);
     if (pend_k >= 0) {   // the one call site of the K3 compute
-      k3_bulk_finish(a, x.slot, x.mtb, x.excl, S.th, x.yt, x.ytl, pend_k, pend_r, x.lane, x.kbuf + pend_b * 4096,
+      k3_bulk_finish(a, x.slot, x.mtb, x.excl, S.th, x.yt, x.ytl, pend_k, pend_r, x.lane, x.kbuf + pend_b * kK3Bytes,
                      &x.kbar[pend_b], par[pend_b]);
       par[pend_b] ^= 1u;
       pend_k = -1;
@@ -858,7 +866,7 @@ __device__ __forceinline__ void aux_prologue(const PipeArgs& a, PipeSmem& S, int
   named_bar(bar, n);
 }
 
-__global__ void __launch_bounds__(kK1Threads, 1) pipe_kernel(const __grid_constant__ PipeArgs a,
+__global__ void __launch_bounds__(kPipeThreads, 1) pipe_kernel(const __grid_constant__ PipeArgs a,
                                                              const __grid_constant__ CUtensorMap rgb_map) {
   extern __shared__ __align__(128) uint8_t pipe_smem_raw[];
   const uint32_t raw = smem_addr(pipe_smem_raw);
@@ -870,7 +878,7 @@ __global__ void __launch_bounds__(kK1Threads, 1) pipe_kernel(const __grid_consta
   // launch may be scheduled as soon as this one's CTAs are all resident.
   grid_dep_launch();
   auto stamp = [&](int i) {
-    if (a.trace && (tid & 255) == 0) {
+    if (a.trace && (tid == 0 || tid == 32 * kPK1Warps)) {
       unsigned long long t;
       asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
       a.trace[((int64_t)a.j * gridDim.x + blockIdx.x) * 16 + i] = t;
@@ -965,37 +973,40 @@ __global__ void __launch_bounds__(kK1Threads, 1) pipe_kernel(const __grid_consta
         if (c) atomicAdd(&gh[(int64_t)i * kHistStrideK1], c);
       }
       // The last CTA to finish image k1_img publishes its medians
-      // (threshold.py:31-39).  Counter: word 1 of bin 0's 128-B line.
-      named_bar(5, 32 * kPK1Warps);
-      if (kt == 0) {
-        __threadfence();
-        S.last = atomicAdd(gh + 1, 1u) == gridDim.x - 1;
-      }
-      named_bar(5, 32 * kPK1Warps);
-      if (S.last) {
-        __threadfence();
-        if (warp < a.n) {
-          const int m = warp_median(gh + warp * 256 * kHistStrideK1, lane);
-          if (lane == 0) a.medians[a.k1_img * a.n + warp] = m;
-        }
-        named_bar(5, 32 * kPK1Warps);
-        if (kt == 0) {
+      // (threshold.py:31-39); only warp 0 waits on the counter (word 1 of
+      // bin 0's 128-B line), the other K1 warps move on to the aux work.
+      named_bar(5, 32 * kPK1Warps);   // every RED of this CTA issued
+      if (warp == 0) {
+        int last = 0;
+        if (lane == 0) {
           __threadfence();
-          atomicExch(a.med_ready + a.k1_img, 1u);
+          last = atomicAdd(gh + 1, 1u) == gridDim.x - 1;
+        }
+        last = __shfl_sync(0xffffffffu, last, 0);
+        if (last) {
+          __threadfence();
+          for (int k = 0; k < a.n; ++k) {
+            const int m = warp_median(gh + k * 256 * kHistStrideK1, lane);
+            if (lane == 0) a.medians[a.k1_img * a.n + k] = m;
+          }
+          if (lane == 0) {
+            __threadfence();
+            atomicExch(a.med_ready + a.k1_img, 1u);
+          }
         }
       }
       stamp(2);
     }
     // Join the aux work.
     if constexpr (kPAuxWarps > 0) {
-      asm volatile("bar.sync 9, %0;" ::"r"(kK1Threads) : "memory");   // S.th / S.next ready
+      asm volatile("bar.sync 9, %0;" ::"r"(kPipeThreads) : "memory");   // S.th / S.next ready
     } else {
-      aux_prologue(a, S, tid, kK1Threads, 9);
+      aux_prologue(a, S, tid, kPipeThreads, 9);
     }
   } else {
     // ======================= aux warps: K3 + search ==========================
     aux_prologue(a, S, tid - 32 * kPK1Warps, 32 * kPAuxWarps, 6);
-    asm volatile("bar.arrive 9, %0;" ::"r"(kK1Threads) : "memory");
+    asm volatile("bar.arrive 9, %0;" ::"r"(kPipeThreads) : "memory");
   }
 
   // ============ every warp: this CTA's share of the aux tasks ================
@@ -1016,7 +1027,7 @@ __global__ void __launch_bounds__(kK1Threads, 1) pipe_kernel(const __grid_consta
   ax.tracer = true;
   if (a.probe != 2) aux_drain(a, S, ax);
   stamp(warp < kPK1Warps ? 3 : 5);
-  named_bar(10, kK1Threads);   // every task of this CTA done
+  named_bar(10, kPipeThreads);   // every task of this CTA done
   if (tid == 0 && a.th_img >= 0) {
     __threadfence();
     atomicAdd(a.k3_done + a.th_img, 1u);
@@ -1154,7 +1165,7 @@ extern "C" int mtb_align_fused(const uint8_t* rgb, int64_t rgb_pitch, int64_t rg
   a.decided = a.k3_done + n_img;
   a.n_launch = J;
   int search_tiles_level[kPipeMaxLevels];
-  for (int k = 0; k < p.n; ++k) search_tiles_level[k] = ((p.lv[k].h + 7) / 8) * ((a.nw32[k] + 31) / 32);
+  for (int k = 0; k < p.n; ++k) search_tiles_level[k] = ((p.lv[k].h + kSRows - 1) / kSRows) * ((a.nw32[k] + 31) / 32);
 
   CUtensorMap map;
   {
@@ -1197,7 +1208,7 @@ extern "C" int mtb_align_fused(const uint8_t* rgb, int64_t rgb_pitch, int64_t rg
     }
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3((unsigned)grid);
-    cfg.blockDim = dim3(kK1Threads);
+    cfg.blockDim = dim3(kPipeThreads);
     cfg.dynamicSmemBytes = kPipeSmemBytes;
     cfg.stream = st;
     cudaLaunchAttribute attr[1];
