@@ -45,7 +45,7 @@ def parse():
     ap.add_argument("--steps", type=int, default=200)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", choices=("ours", "reference"), default="ours")
-    ap.add_argument("--pairs", type=int, default=16, help="pairs per step per GPU")
+    ap.add_argument("--pairs", type=int, default=32, help="pairs per step per GPU")
     ap.add_argument("--width", type=int, default=6000)
     ap.add_argument("--height", type=int, default=4000)
     ap.add_argument("--levels", type=int, default=6)

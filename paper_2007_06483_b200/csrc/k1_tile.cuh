@@ -233,12 +233,28 @@ __host__ __device__ constexpr int tm_off(int k) {
 __host__ __device__ constexpr int tm_pitch(int k) { return 256 >> k; }
 constexpr int kTileGrayBytes = 11008;                                // 86 x 128 B
 
+// Tile-major gray stores.  With PIPE_GRAY_EVICT_LAST the level-0/1 stores
+// carry an L2::evict_last policy (the gray is read back one launch later).
+#ifdef PIPE_GRAY_EVICT_LAST
+#define TM_POL , uint64_t gpol
+#define TM_POLARG , gpol
+__device__ __forceinline__ void st8(uint8_t* p, uint32_t a, uint32_t b, uint64_t pol) {
+  asm volatile("st.global.L2::cache_hint.v2.u32 [%0], {%1, %2}, %3;" ::"l"(p), "r"(a), "r"(b), "l"(pol) : "memory");
+}
+__device__ __forceinline__ void st4p(uint8_t* p, uint32_t a, uint64_t pol) {
+  asm volatile("st.global.L2::cache_hint.u32 [%0], %1, %2;" ::"l"(p), "r"(a), "l"(pol) : "memory");
+}
+#else
+#define TM_POL
+#define TM_POLARG
 __device__ __forceinline__ void st8(uint8_t* p, uint32_t a, uint32_t b) { *reinterpret_cast<uint2*>(p) = make_uint2(a, b); }
+__device__ __forceinline__ void st4p(uint8_t* p, uint32_t a) { *reinterpret_cast<uint32_t*>(p) = a; }
+#endif
 
 // k1_block for the tile-major layout: `tg` = this tile's gray region.
 template <bool FULL>
 __device__ __forceinline__ void k1_block_tm(const K1Args& a, uint8_t* tg, const uint2 (&v)[8][3], int tx, int ty,
-                                            int wg, int lane, uint32_t hb, uint8_t* l3_slot) {
+                                            int wg, int lane, uint32_t hb, uint8_t* l3_slot TM_POL) {
   const int x0 = tx * kK1TilePx + 8 * lane;
   const int y0 = ty * kK1TileRows + 8 * wg;
   uint32_t l1[4];
@@ -262,7 +278,7 @@ __device__ __forceinline__ void k1_block_tm(const K1Args& a, uint8_t* tg, const 
           if (FULL || (row_ok && i < nv0)) hinc(hb | ((sa[i] >> 6) & 0x3fcu));
           if (FULL || (row_ok && 4 + i < nv0)) hinc(hb | ((sb[i] >> 6) & 0x3fcu));
         }
-        st8(p0 + r * tm_pitch(0), gw[j][0], gw[j][1]);
+        st8(p0 + r * tm_pitch(0), gw[j][0], gw[j][1] TM_POLARG);
       }
       if (a.nl >= 2) {
         const uint32_t s0 = box_sum(gw[0][0], gw[1][0], 0), s1 = box_sum(gw[0][0], gw[1][0], 1);
@@ -275,7 +291,7 @@ __device__ __forceinline__ void k1_block_tm(const K1Args& a, uint8_t* tg, const 
         if (FULL || (row_ok && 3 < nv1)) hinc(hb1 | (s3 & 0x3fcu));
         const uint32_t x01 = (s0 + (s1 << 16)) >> 2, x23 = (s2 + (s3 << 16)) >> 2;
         l1[rp] = __byte_perm(x01, x23, 0x6420);
-        *reinterpret_cast<uint32_t*>(p1 + rp * tm_pitch(1)) = l1[rp];
+        st4p(p1 + rp * tm_pitch(1), l1[rp] TM_POLARG);
       }
     }
   }

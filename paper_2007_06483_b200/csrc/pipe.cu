@@ -26,6 +26,12 @@
 #include <cstring>
 #include <vector>
 
+// Level-0/1 gray is stored with L2::evict_last (no persisting set-aside: it
+// measured slower); the RGB stream is evict_first.
+#ifndef PIPE_GRAY_EVICT_NORMAL
+#define PIPE_GRAY_EVICT_LAST
+#endif
+
 #include "k1_tile.cuh"
 #include "swar.cuh"
 
@@ -898,6 +904,10 @@ __global__ void __launch_bounds__(kPipeThreads, 1) pipe_kernel(const __grid_cons
       uint32_t* ctr = a.ctr + a.j;   // K1 tile counter of this launch
       uint64_t pol_first;
       asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol_first));
+#ifdef PIPE_GRAY_EVICT_LAST
+      uint64_t gpol;
+      asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(gpol));
+#endif
       for (int i = kt; i < 6 * 256; i += 32 * kPK1Warps) (&S.hist[0][0])[i] = 0;
       // Claim the next tile of the image for ring stage `stage` (launch-wide
       // counter: CTAs that start late take fewer tiles) and start its copy;
@@ -953,9 +963,9 @@ __global__ void __launch_bounds__(kPipeThreads, 1) pipe_kernel(const __grid_cons
         uint8_t* tg = slot + (int64_t)tile * kTileGrayBytes;
         uint8_t* l3_slot = &S.l3[g][k & 1][wg][lane];
         if (full)
-          k1_block_tm<true>(a.g, tg, v, tx, ty, wg, lane, hb, l3_slot);
+          k1_block_tm<true>(a.g, tg, v, tx, ty, wg, lane, hb, l3_slot TM_POLARG);
         else
-          k1_block_tm<false>(a.g, tg, v, tx, ty, wg, lane, hb, l3_slot);
+          k1_block_tm<false>(a.g, tg, v, tx, ty, wg, lane, hb, l3_slot TM_POLARG);
         ptx = tx;
         pty = ty;
         ptile = tile;
