@@ -557,31 +557,43 @@ __device__ __forceinline__ void pipe_search_tile(const PipeArgs& a, const PipeIt
   // ---- stage: A/EA rows y0..y0+7, words j0..j0+31; B/EB source rows
   //      y0-by-1 .. y0-by+8, words j0-qb-2 .. j0-qb+32
   {
+    // Running row pointers; a copy with src-size 0 reads nothing and
+    // zero-fills, so out-of-map rows/words need no address clamping.
     const int j = j0 + lane;
+    const bool colA = j < nw;
+    const int ja = colA ? j : 0;
+    const uint32_t* pa = A + (int64_t)y0 * nw + ja;
+    const uint32_t* pea = EA + (int64_t)y0 * nw + ja;
 #pragma unroll
     for (int r = 0; r < kSRows; ++r) {
-      const int y = y0 + r;
-      const bool ok = y < h && j < nw;
-      const int64_t o = ok ? (int64_t)y * nw + j : 0;
-      cp_async4(&sm.a[r][lane], A + o, ok);
-      cp_async4(&sm.ea[r][lane], EA + o, ok);
+      const bool ok = colA && (y0 + r < h);
+      cp_async4(&sm.a[r][lane], pa, ok);
+      cp_async4(&sm.ea[r][lane], pea, ok);
+      pa += nw;
+      pea += nw;
     }
     const int sy0 = y0 - by - 1;
+    const int idx0 = j0 - qb - 2 + lane, idx1 = idx0 + 32;
+    const bool c0 = idx0 >= 0 && idx0 < nw, c1 = lane < 3 && idx1 >= 0 && idx1 < nw;
+    const int64_t rowoff = (int64_t)sy0 * nw;
+    const uint32_t* pb0 = B + rowoff + (c0 ? idx0 : 0);
+    const uint32_t* peb0 = EB + rowoff + (c0 ? idx0 : 0);
+    const uint32_t* pb1 = B + rowoff + (c1 ? idx1 : 0);
+    const uint32_t* peb1 = EB + rowoff + (c1 ? idx1 : 0);
 #pragma unroll
     for (int r = 0; r < kSRows + 2; ++r) {
       const int sy = sy0 + r;
       const bool rok = sy >= 0 && sy < h;
-#pragma unroll
-      for (int c = 0; c < 2; ++c) {
-        const int col = lane + 32 * c;
-        if (c == 0 || col < 35) {
-          const int idx = j0 - qb - 2 + col;
-          const bool ok = rok && idx >= 0 && idx < nw;
-          const int64_t o = ok ? (int64_t)sy * nw + idx : 0;
-          cp_async4(&sm.b[r][col], B + o, ok);
-          cp_async4(&sm.eb[r][col], EB + o, ok);
-        }
+      cp_async4(&sm.b[r][lane], pb0, rok && c0);
+      cp_async4(&sm.eb[r][lane], peb0, rok && c0);
+      if (lane < 3) {
+        cp_async4(&sm.b[r][lane + 32], pb1, rok && c1);
+        cp_async4(&sm.eb[r][lane + 32], peb1, rok && c1);
       }
+      pb0 += nw;
+      peb0 += nw;
+      pb1 += nw;
+      peb1 += nw;
     }
     asm volatile("cp.async.wait_all;" ::: "memory");
     __syncwarp();
