@@ -24,6 +24,7 @@
 // round trip (32 MB per 24 MP image) stays in L2.
 #include <cstdlib>
 #include <cstring>
+#include <type_traits>
 #include <vector>
 
 // Level-0/1 gray is stored with L2::evict_last (no persisting set-aside: it
@@ -598,55 +599,63 @@ __device__ __forceinline__ void pipe_search_tile(const PipeArgs& a, const PipeIt
     asm volatile("cp.async.wait_all;" ::: "memory");
     __syncwarp();
   }
-  int o[3], r[3];
-#pragma unroll
-  for (int d = 0; d < 3; ++d) {
-    const int dx = bx + d - 1;
-    o[d] = (dx >> 5) - qb;   // in {-1, 0, 1}
-    r[d] = dx & 31;
-  }
-  // staged source row lr shifted by bx-1, bx, bx+1: W[j-q] = w[2-o], W[j-q-1] = w[1-o], w[i] = staged word lane+i
-  auto shifted = [&](int lr, uint32_t (&sb)[3], uint32_t (&se)[3]) {
-    uint32_t wb[4], we[4];
-#pragma unroll
-    for (int i = 0; i < 4; ++i) {
-      wb[i] = sm.b[lr][lane + i];
-      we[i] = sm.eb[lr][lane + i];
-    }
-#pragma unroll
-    for (int d = 0; d < 3; ++d) {
-      const uint32_t hb = o[d] < 0 ? wb[3] : (o[d] == 0 ? wb[2] : wb[1]);
-      const uint32_t lb = o[d] < 0 ? wb[2] : (o[d] == 0 ? wb[1] : wb[0]);
-      const uint32_t he = o[d] < 0 ? we[3] : (o[d] == 0 ? we[2] : we[1]);
-      const uint32_t le = o[d] < 0 ? we[2] : (o[d] == 0 ? we[1] : we[0]);
-      sb[d] = shifted_word(lb, hb, r[d]);
-      se[d] = shifted_word(le, he, r[d]);
-    }
-  };
+  // Candidate ddx = d - 1 shifts the target by dx = bx + d - 1 = 32 q + r.
+  // With qb = bx >> 5 and rb = bx & 31 only three word selections occur
+  // (staged word w[i] = lane + i holds W[j - qb - 2 + i]):
+  //   rb == 0 : d=0 -> (w2, w3) r=31, d=1 -> (w1, w2) r=0,  d=2 -> (w1, w2) r=1
+  //   rb == 31: d=0 -> (w1, w2) r=30, d=1 -> (w1, w2) r=31, d=2 -> (w0, w1) r=0
+  //   else    : d   -> (w1, w2) r = rb + d - 1   (rb = rbx below)
+  // so the row loop is instantiated per case without per-lane selects.
+  const int rbx = bx & 31;
   unsigned cnt[9];
 #pragma unroll
   for (int i = 0; i < 9; ++i) cnt[i] = 0;
-  // output row y0+rr needs staged source rows rr+2 (ddy=-1), rr+1 (0), rr (+1)
-  uint32_t b0[3], e0[3], b1[3], e1[3];
-  shifted(0, b0, e0);
-  shifted(1, b1, e1);
+  auto rows = [&](auto case_tag) {
+    constexpr int CASE = decltype(case_tag)::value;   // 0: rb==0, 1: rb==31, 2: other
+    const int r0 = CASE == 0 ? 31 : (CASE == 1 ? 30 : rbx - 1);
+    const int r1 = CASE == 0 ? 0 : (CASE == 1 ? 31 : rbx);
+    const int r2 = CASE == 0 ? 1 : (CASE == 1 ? 0 : rbx + 1);
+    auto shifted = [&](int lr, uint32_t (&sb)[3], uint32_t (&se)[3]) {
+      const uint32_t b0 = sm.b[lr][lane], b1 = sm.b[lr][lane + 1], b2 = sm.b[lr][lane + 2];
+      const uint32_t e0 = sm.eb[lr][lane], e1 = sm.eb[lr][lane + 1], e2 = sm.eb[lr][lane + 2];
+      if (CASE == 0) {
+        const uint32_t b3 = sm.b[lr][lane + 3], e3 = sm.eb[lr][lane + 3];
+        sb[0] = shifted_word(b2, b3, r0); se[0] = shifted_word(e2, e3, r0);
+      } else {
+        sb[0] = shifted_word(b1, b2, r0); se[0] = shifted_word(e1, e2, r0);
+      }
+      sb[1] = shifted_word(b1, b2, r1); se[1] = shifted_word(e1, e2, r1);
+      if (CASE == 1) {
+        sb[2] = shifted_word(b0, b1, r2); se[2] = shifted_word(e0, e1, r2);
+      } else {
+        sb[2] = shifted_word(b1, b2, r2); se[2] = shifted_word(e1, e2, r2);
+      }
+    };
+    // output row y0+rr needs staged source rows rr+2 (ddy=-1), rr+1 (0), rr (+1)
+    uint32_t b0[3], e0[3], b1[3], e1[3];
+    shifted(0, b0, e0);
+    shifted(1, b1, e1);
 #pragma unroll 2
-  for (int rr = 0; rr < kSRows; ++rr) {
-    uint32_t b2[3], e2[3];
-    shifted(rr + 2, b2, e2);
-    const uint32_t av = sm.a[rr][lane], ev = sm.ea[rr][lane];
+    for (int rr = 0; rr < kSRows; ++rr) {
+      uint32_t b2[3], e2[3];
+      shifted(rr + 2, b2, e2);
+      const uint32_t av = sm.a[rr][lane], ev = sm.ea[rr][lane];
 #pragma unroll
-    for (int d = 0; d < 3; ++d) {
-      cnt[0 + d] += __popc((av ^ b2[d]) & ev & e2[d]);
-      cnt[3 + d] += __popc((av ^ b1[d]) & ev & e1[d]);
-      cnt[6 + d] += __popc((av ^ b0[d]) & ev & e0[d]);
-    }
+      for (int d = 0; d < 3; ++d) {
+        cnt[0 + d] += __popc((av ^ b2[d]) & ev & e2[d]);
+        cnt[3 + d] += __popc((av ^ b1[d]) & ev & e1[d]);
+        cnt[6 + d] += __popc((av ^ b0[d]) & ev & e0[d]);
+      }
 #pragma unroll
-    for (int d = 0; d < 3; ++d) {
-      b0[d] = b1[d]; e0[d] = e1[d];
-      b1[d] = b2[d]; e1[d] = e2[d];
+      for (int d = 0; d < 3; ++d) {
+        b0[d] = b1[d]; e0[d] = e1[d];
+        b1[d] = b2[d]; e1[d] = e2[d];
+      }
     }
-  }
+  };
+  if (rbx == 0) rows(std::integral_constant<int, 0>{});
+  else if (rbx == 31) rows(std::integral_constant<int, 1>{});
+  else rows(std::integral_constant<int, 2>{});
   __syncwarp();   // the staging buffer is reused by the next tile
   // CTA-level partial counts (shared atomics); flushed once per CTA and item
   // by pipe_search_flush after all of the CTA's tasks are done.
