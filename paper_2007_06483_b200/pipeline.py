@@ -206,8 +206,11 @@ def get_exp_shift(ref_rgb, tgt_rgb, levels: int = DEFAULT_LEVELS, tol: int = DEF
     w, h = _validate_stack([ref_rgb, tgt_rgb])
     eng = engine_for(w, h, levels, tol)
     batch = upload_stack([ref_rgb, tgt_rgb])
-    pyr = eng.preprocess(batch)
-    acc, _ = eng.search(pyr, [(0, 1)])
+    if eng.fused_supported:
+        _, acc, _ = eng.align_fused(batch, [(0, 1)])     # one pipelined launch sequence (csrc/pipe.cu)
+    else:
+        pyr = eng.preprocess(batch)
+        acc, _ = eng.search(pyr, [(0, 1)])
     a = acc[0, 0].cpu().numpy()
     return ShiftOffset(int(a[0]), int(a[1]))
 

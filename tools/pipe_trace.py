@@ -43,29 +43,14 @@ for j in range(J):
              f"{us(r[:, 5]).max():8.1f}  aux max {((r[:, 5] - r[:, 4]) / 1e3).max():5.1f}")
     print(line)
 
-# stragglers: per CTA aux durations in K1 launches 10..30
-aux = (t[10:31, :, 5] - t[10:31, :, 4]) / 1e3
-k1a = (t[10:31, :, 3] - t[10:31, :, 1]) / 1e3
-sm = t[10:31, :, 6]
-print("aux per CTA: median over launches, top 12 slow CTAs (cta, smid, aux_med, k1aux_med)")
-rot = int(os.environ.get("MTB_PIPE_ROT", "0"))
-if rot:
-    slice_of = np.array([[(c + rot * j) % G for c in range(G)] for j in range(10, 31)])
-    aux_s = np.zeros(G)
-    for jj in range(aux.shape[0]):
-        aux_s[slice_of[jj]] = aux[jj]
-    print("by slice (last launch): slowest slices", np.argsort(-aux_s)[:5], "by SM:", [int(sm[-1, c]) for c in np.argsort(-aux[-1])[:5]])
-    print("per launch slowest (cta, slice, smid):", [(int(np.argmax(aux[jj])), int(slice_of[jj][np.argmax(aux[jj])]), int(sm[jj, np.argmax(aux[jj])]), round(float(aux[jj].max()),1)) for jj in range(0, 21, 3)])
-med = np.median(aux, axis=0)
-order = np.argsort(-med)
-for c in order[:12]:
-    print(c, int(sm[0, c]), round(float(med[c]), 1), round(float(np.median(k1a[:, c])), 1))
-print("fast CTAs", [(int(c), int(sm[0, c]), round(float(med[c]), 1)) for c in order[-6:]])
-print("corr of aux time between consecutive launches", np.corrcoef(aux[:-1].ravel(), aux[1:].ravel())[0, 1])
-
-print("phase start offsets (us after aux start) for CTA 147 vs CTA 5, launches 20..23; phases 0..6, then aux end")
+# phase starts (first task of each aux phase in the CTA) relative to the CTA's K1 start, launches 20..23
+names = {6: "search", 0: "K3 L0", 1: "K3 L1", 2: "K3 L2", 3: "K3 L3", 4: "L4-5", 5: "pad"}
 for j in range(20, 24):
-    for c in (147, 5):
-        r = t[j, c]
-        ph = [round((r[8 + p] - r[4]) / 1e3, 1) if r[8 + p] else None for p in range(7)]
-        print(j, c, ph, round((r[5] - r[4]) / 1e3, 1))
+    r = t[j]
+    row = []
+    for p in (6, 0, 1, 2, 3, 4):
+        v = r[:, 8 + p]
+        ok = v > 0
+        row.append(f"{names[p]} {np.median((v[ok] - r[ok, 0]) / 1e3):6.1f}" if ok.any() else f"{names[p]}   -  ")
+    end = np.median((np.maximum(r[:, 3], r[:, 5]) - r[:, 0]) / 1e3)
+    print(j, " | ".join(row), f"| end {end:6.1f} | k1 tiles end {np.median((r[:, 1] - r[:, 0]) / 1e3):6.1f}")
