@@ -134,6 +134,7 @@ struct PipeSmem {
   int next;                                               // aux task queue head
   int plo[kAuxPhases], pcnt[kAuxPhases];                  // this CTA's slice of each aux phase
   int sleft;                                              // this CTA's search tiles not yet done
+  int th_state;                                           // 0 idle, 1 being filled, 2 S.th valid
   unsigned scnt[kPipeMaxItems][9];                        // per-item partial search counts
 };
 constexpr int kPipeSmemBytes = (int)sizeof(PipeSmem) + 1024;
@@ -797,6 +798,48 @@ __device__ __forceinline__ void aux_run(const PipeArgs& a, PipeSmem& S, const Au
 // next launch's level can start early), then K3 levels 0..3, 4..5, padding.
 __device__ __forceinline__ int aux_phase_of(const PipeArgs& a, int q) { return q == 0 ? 6 : q - 1; }
 
+__device__ __forceinline__ void aux_stamp(const PipeArgs& a, int i) {
+  if (a.trace) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+    a.trace[((int64_t)a.j * gridDim.x + blockIdx.x) * 16 + i] = t;
+  }
+}
+
+// The threshold constants of image th_img are needed only by K3 and level
+// 4-5 tasks, and only once image th_img's medians are published: the first
+// warp to reach such a task waits for them and fills S.th; others wait on
+// S.th_state.  Search tasks (first in the queue) run meanwhile.
+__device__ __forceinline__ void aux_need_thresholds(const PipeArgs& a, PipeSmem& S, int lane) {
+  volatile int* st = &S.th_state;
+  if (*st == 2) return;
+  int claim = 0;
+  if (lane == 0) claim = atomicCAS(&S.th_state, 0, 1) == 0;
+  claim = __shfl_sync(0xffffffffu, claim, 0);
+  if (claim) {
+    if (lane == 0) spin_geq(a.med_ready + a.th_img, 1u);
+    __syncwarp();
+    if (lane < a.n) {
+      const int med = __ldcg(a.medians + a.th_img * a.n + lane);
+      ThConst c;
+      c.med = (uint32_t)med * 0x01010101u;
+      c.ym = (uint32_t)(255 - med) * 0x01010101u;
+      c.yml = c.ym & 0x7f7f7f7fu;
+      c.med_lo = med <= 127;
+      S.th[lane] = c;
+    }
+    __threadfence_block();
+    __syncwarp();
+    if (lane == 0) {
+      *st = 2;
+      aux_stamp(a, 5);
+    }
+  } else {
+    while (*st != 2) __nanosleep(32);
+  }
+  __threadfence_block();
+}
+
 __device__ __forceinline__ void aux_drain(const PipeArgs& a, PipeSmem& S, const AuxCtx& x) {
   int lo[kAuxPhases], cnt[kAuxPhases];   // this CTA's slices in queue order (aux prologue)
 #pragma unroll
@@ -830,6 +873,7 @@ __device__ __forceinline__ void aux_drain(const PipeArgs& a, PipeSmem& S, const 
       }
     }
     const bool k3 = p >= 0 && p < 4;
+    if (k3) aux_need_thresholds(a, S, x.lane);
     if (k3) k3_bulk_issue(a, x.slot, p, r, x.lane, x.kbuf + nb * kK3Bytes, &x.kbar[nb]);
     if (pend_k >= 0) {   // the one call site of the K3 compute
       k3_bulk_finish(a, x.slot, x.mtb, x.excl, S.th, x.yt, x.ytl, pend_k, pend_r, x.lane, x.kbuf + pend_b * kK3Bytes,
@@ -845,6 +889,7 @@ __device__ __forceinline__ void aux_drain(const PipeArgs& a, PipeSmem& S, const 
       continue;
     }
     if (p < 0) return;
+    if (p == 4) aux_need_thresholds(a, S, x.lane);
     aux_run(a, S, x, p, r);
     if (p == 6) {
       // last search tile of this CTA: publish its partial counts
@@ -867,17 +912,7 @@ __device__ __forceinline__ void aux_drain(const PipeArgs& a, PipeSmem& S, const 
 // (spin), threshold constants, the CTA's task slices, queue and search
 // counters reset.  Run by `n` threads (at = 0..n-1) synchronised on `bar`.
 __device__ __forceinline__ void aux_prologue(const PipeArgs& a, PipeSmem& S, int at, int n, int bar) {
-  if (at == 0 && a.th_img >= 0) spin_geq(a.med_ready + a.th_img, 1u);   // image th_img's K1 published
-  named_bar(bar, n);
-  if (a.th_img >= 0 && at < a.n) {
-    const int med = __ldcg(a.medians + a.th_img * a.n + at);
-    ThConst c;
-    c.med = (uint32_t)med * 0x01010101u;
-    c.ym = (uint32_t)(255 - med) * 0x01010101u;
-    c.yml = c.ym & 0x7f7f7f7fu;
-    c.med_lo = med <= 127;
-    S.th[at] = c;
-  }
+  if (at == 0) S.th_state = 0;
   if (at == 0) S.next = 0;
   if (at < kAuxPhases) {
     const int G = gridDim.x, c = blockIdx.x;

@@ -54,3 +54,5 @@ for j in range(20, 24):
         row.append(f"{names[p]} {np.median((v[ok] - r[ok, 0]) / 1e3):6.1f}" if ok.any() else f"{names[p]}   -  ")
     end = np.median((np.maximum(r[:, 3], r[:, 5]) - r[:, 0]) / 1e3)
     print(j, " | ".join(row), f"| end {end:6.1f} | k1 tiles end {np.median((r[:, 1] - r[:, 0]) / 1e3):6.1f}")
+    pro = [np.median((r[:, i] - r[:, 0]) / 1e3) for i in (4, 5, 6, 7)]
+    print("   aux prologue: start %.1f  med_ready %.1f  consts %.1f  done %.1f" % tuple(pro))
