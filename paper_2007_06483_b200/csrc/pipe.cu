@@ -135,6 +135,8 @@ struct PipeSmem {
   int plo[kAuxPhases], pcnt[kAuxPhases];                  // this CTA's slice of each aux phase
   int sleft;                                              // this CTA's search tiles not yet done
   int th_state;                                           // 0 idle, 1 being filled, 2 S.th valid
+  int k1_warps_done;                                      // K1 warps past their last tile
+  int aux_ready;                                          // aux prologue done (queue + slices valid)
   unsigned scnt[kPipeMaxItems][9];                        // per-item partial search counts
 };
 constexpr int kPipeSmemBytes = (int)sizeof(PipeSmem) + 1024;
@@ -912,7 +914,6 @@ __device__ __forceinline__ void aux_drain(const PipeArgs& a, PipeSmem& S, const 
 // (spin), threshold constants, the CTA's task slices, queue and search
 // counters reset.  Run by `n` threads (at = 0..n-1) synchronised on `bar`.
 __device__ __forceinline__ void aux_prologue(const PipeArgs& a, PipeSmem& S, int at, int n, int bar) {
-  if (at == 0) S.th_state = 0;
   if (at == 0) S.next = 0;
   if (at < kAuxPhases) {
     const int G = gridDim.x, c = blockIdx.x;
@@ -939,6 +940,12 @@ __global__ void __launch_bounds__(kPipeThreads, 1) pipe_kernel(const __grid_cons
   // All dependencies on earlier launches are explicit flags, so the next
   // launch may be scheduled as soon as this one's CTAs are all resident.
   grid_dep_launch();
+  if (tid == 0) {   // control words read across warp roles (smem is not zeroed between CTAs)
+    S.aux_ready = 0;
+    S.k1_warps_done = 0;
+    S.th_state = 0;
+  }
+  __syncthreads();
   auto stamp = [&](int i) {
     if (a.trace && (tid == 0 || tid == 32 * kPK1Warps)) {
       unsigned long long t;
@@ -1031,18 +1038,24 @@ __global__ void __launch_bounds__(kPipeThreads, 1) pipe_kernel(const __grid_cons
       if (k > 0 && a.g.nl >= 5 && wg == ((k - 1) & 3))
         k1_levels45_tm(a.g, slot + (int64_t)ptile * kTileGrayBytes, S.l3[g][(k - 1) & 1], ptx, pty, lane, hb,
                        pfull);
-      named_bar(5, 32 * kPK1Warps);
+      // The last K1 warp of the CTA to finish flushes the CTA's histograms;
+      // if this is the last CTA of image k1_img it also publishes the medians
+      // (threshold.py:31-39).  Counter: word 1 of bin 0's 128-B line.  The
+      // other K1 warps go straight to the aux work.
       stamp(1);
-      uint32_t* gh = a.g.hist + (int64_t)a.k1_img * a.g.hist_img_stride;
-      for (int i = kt; i < a.g.nl * 256; i += 32 * kPK1Warps) {
-        const uint32_t c = (&S.hist[0][0])[i];
-        if (c) atomicAdd(&gh[(int64_t)i * kHistStrideK1], c);
+      int mine = 0;
+      if (lane == 0) {
+        __threadfence_block();
+        mine = atomicAdd(&S.k1_warps_done, 1) == kPK1Warps - 1;
       }
-      // The last CTA to finish image k1_img publishes its medians
-      // (threshold.py:31-39); only warp 0 waits on the counter (word 1 of
-      // bin 0's 128-B line), the other K1 warps move on to the aux work.
-      named_bar(5, 32 * kPK1Warps);   // every RED of this CTA issued
-      if (warp == 0) {
+      mine = __shfl_sync(0xffffffffu, mine, 0);
+      if (mine) {
+        __threadfence_block();
+        uint32_t* gh = a.g.hist + (int64_t)a.k1_img * a.g.hist_img_stride;
+        for (int i = lane; i < a.g.nl * 256; i += 32) {
+          const uint32_t c = *reinterpret_cast<volatile uint32_t*>(&(&S.hist[0][0])[i]);
+          if (c) atomicAdd(&gh[(int64_t)i * kHistStrideK1], c);
+        }
         int last = 0;
         if (lane == 0) {
           __threadfence();
@@ -1060,19 +1073,23 @@ __global__ void __launch_bounds__(kPipeThreads, 1) pipe_kernel(const __grid_cons
             atomicExch(a.med_ready + a.k1_img, 1u);
           }
         }
+        stamp(2);
       }
-      stamp(2);
     }
-    // Join the aux work.
+    // Join the aux work (the aux prologue has long finished: spin on its flag).
     if constexpr (kPAuxWarps > 0) {
-      asm volatile("bar.sync 9, %0;" ::"r"(kPipeThreads) : "memory");   // S.th / S.next ready
+      while (*reinterpret_cast<volatile int*>(&S.aux_ready) == 0) __nanosleep(64);
+      __threadfence_block();
     } else {
       aux_prologue(a, S, tid, kPipeThreads, 9);
     }
   } else {
     // ======================= aux warps: K3 + search ==========================
     aux_prologue(a, S, tid - 32 * kPK1Warps, 32 * kPAuxWarps, 6);
-    asm volatile("bar.arrive 9, %0;" ::"r"(kPipeThreads) : "memory");
+    if (tid == 32 * kPK1Warps) {
+      __threadfence_block();
+      *reinterpret_cast<volatile int*>(&S.aux_ready) = 1;
+    }
   }
 
   // ============ every warp: this CTA's share of the aux tasks ================
