@@ -385,6 +385,18 @@ __device__ __forceinline__ void k3_finish(const uint8_t* slot, uint32_t* mtb, ui
 // while task r+1 is in flight, without holding it in registers.
 __device__ __forceinline__ void k3_bulk_issue(const PipeArgs& a, const uint8_t* slot, int K, int r, int lane,
                                               uint8_t* buf, unsigned long long* bar) {
+  if (K == 0) {   // one contiguous 4 KB half-tile
+    if (lane == 0) {
+      mbar_expect_tx(bar, (uint32_t)kK3Bytes);
+      const uint8_t* src = slot + (int64_t)(r >> 1) * kTileGrayBytes + (r & 1) * kK3Bytes;
+      asm volatile(
+          "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+              smem_addr(buf)),
+          "l"(src), "r"(kK3Bytes), "r"(smem_addr(bar))
+          : "memory");
+    }
+    return;
+  }
   const int lwpt = 8 - 2 * K;
   const int wpt = 1 << lwpt;
   const int pw = wpt < kK3Words ? wpt : kK3Words;   // words per piece
@@ -446,6 +458,34 @@ __device__ __forceinline__ void k3_bulk_units(const PipeArgs& a, uint32_t* mtb, 
   }
 }
 
+// Level 0: the task is half a tile (rows 16 (r & 1) .. +15, 8 words each);
+// unit i covers rows +4i .. +4i+3, so tile, column and validity are per task.
+template <bool MED_LO>
+__device__ __forceinline__ void k3_bulk_units_l0(const PipeArgs& a, uint32_t* mtb, uint32_t* excl, const ThConst& c,
+                                                 uint32_t yt, uint32_t ytl, int r, int lane, const uint8_t* buf) {
+  const int nw = a.nw32[0], lh = a.g.lh[0];
+  const int t = r >> 1;
+  const int ty = div_tiles_x(a, t), tx = t - ty * a.g.tiles_x;
+  const int j = tx * 8 + (lane & 7);
+  const int y0 = ty * kK1TileRows + ((r & 1) << 4) + (lane >> 3);
+  const int valid = a.g.lw[0] - 32 * j;
+  const bool ok = j < nw;
+  uint32_t* pm = mtb + (int)a.bit_off32[0] + y0 * nw + j;
+  uint32_t* pe = excl + (int)a.bit_off32[0] + y0 * nw + j;
+#pragma unroll
+  for (int i = 0; i < kK3Units; ++i) {
+    const uint4 v0 = *reinterpret_cast<const uint4*>(buf + (i * 32 + lane) * 32);
+    const uint4 v1 = *reinterpret_cast<const uint4*>(buf + (i * 32 + lane) * 32 + 16);
+    const uint32_t g[8] = {v0.x, v0.y, v0.z, v0.w, v1.x, v1.y, v1.z, v1.w};
+    uint32_t m, e;
+    th_word_t<MED_LO, true>(g, c, yt, ytl, valid, m, e);
+    if (ok && y0 + 4 * i < lh) {
+      pm[4 * i * nw] = m;
+      pe[4 * i * nw] = e;
+    }
+  }
+}
+
 __device__ __forceinline__ void k3_bulk_finish(const PipeArgs& a, const uint8_t* slot, uint32_t* mtb, uint32_t* excl,
                                                const ThConst* th, uint32_t yt, uint32_t ytl, int K, int r, int lane,
                                                const uint8_t* buf, unsigned long long* bar, uint32_t parity) {
@@ -472,6 +512,11 @@ __device__ __forceinline__ void k3_bulk_finish(const PipeArgs& a, const uint8_t*
         excl[o] = e;
       }
     }
+  } else if (K == 0) {
+    if (c.med_lo)
+      k3_bulk_units_l0<true>(a, mtb, excl, c, yt, ytl, r, lane, buf);
+    else
+      k3_bulk_units_l0<false>(a, mtb, excl, c, yt, ytl, r, lane, buf);
   } else if (c.med_lo) {
     k3_bulk_units<true>(a, mtb, excl, c, yt, ytl, K, r, lane, buf);
   } else {
@@ -480,7 +525,11 @@ __device__ __forceinline__ void k3_bulk_finish(const PipeArgs& a, const uint8_t*
   const int lwpt = 8 - 2 * K, wpt = 1 << lwpt;
   const int ntiles = a.g.tiles_x * a.g.tiles_y;
   // line `lane` of the task's gray: drop it from L2 without write-back
-  if (lane < kK3Bytes / 128) {
+  if (K == 0) {
+    asm volatile("discard.global.L2 [%0], 128;" ::"l"(slot + (int64_t)(r >> 1) * kTileGrayBytes +
+                                                       (r & 1) * kK3Bytes + lane * 128)
+                 : "memory");
+  } else if (lane < kK3Bytes / 128) {
     const int f = kK3Words * r + 4 * lane;
     const int t = f >> lwpt;
     if (t < ntiles)
