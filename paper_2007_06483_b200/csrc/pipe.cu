@@ -133,6 +133,7 @@ struct PipeSmem {
   int last;
   int next;                                               // aux task queue head
   int plo[kAuxPhases], pcnt[kAuxPhases];                  // this CTA's slice of each aux phase
+  int pend[kAuxPhases], pdelta[kAuxPhases];               // queue index end / task = index + delta
   int sleft;                                              // this CTA's search tiles not yet done
   int th_state;                                           // 0 idle, 1 being filled, 2 S.th valid
   int k1_warps_done;                                      // K1 warps past their last tile
@@ -892,30 +893,24 @@ __device__ __forceinline__ void aux_need_thresholds(const PipeArgs& a, PipeSmem&
 }
 
 __device__ __forceinline__ void aux_drain(const PipeArgs& a, PipeSmem& S, const AuxCtx& x) {
-  int lo[kAuxPhases], cnt[kAuxPhases];   // this CTA's slices in queue order (aux prologue)
-#pragma unroll
-  for (int q = 0; q < kAuxPhases; ++q) {
-    lo[q] = S.plo[q];
-    cnt[q] = S.pcnt[q];
-  }
   if (x.lane == 0) {
     mbar_init(&x.kbar[0], 1);
     mbar_init(&x.kbar[1], 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncwarp();
-  uint32_t par[2] = {0u, 0u};
+  uint32_t par = 0u;                         // mbarrier phase bit per staging buffer
   int pend_k = -1, pend_r = 0, pend_b = 0;   // K3 task in flight
   int nb = 0;                                // next staging buffer
+  int q = 0;                                 // queue phase (a warp's claims only grow)
   for (;;) {
     int t = 0;
-    if (x.lane == 0) t = atomicAdd(&S.next, 1);
+    if (x.lane == 0) asm volatile("atom.shared.add.u32 %0, [%1], 1;" : "=r"(t) : "r"(smem_addr(&S.next)) : "memory");
     t = __shfl_sync(0xffffffffu, t, 0);
-    int q = 0;
-    while (q < kAuxPhases && t >= cnt[q]) t -= cnt[q++];
+    while (q < kAuxPhases && t >= S.pend[q]) ++q;
     const int p = q < kAuxPhases ? aux_phase_of(a, q) : -1;
-    const int r = q < kAuxPhases ? lo[q] + t : 0;
-    if (p >= 0 && x.tracer && x.lane == 0 && a.trace) {
+    const int r = q < kAuxPhases ? t + S.pdelta[q] : 0;
+    if (a.trace && p >= 0 && x.tracer && x.lane == 0) {
       unsigned long long* slot = a.trace + ((int64_t)a.j * gridDim.x + blockIdx.x) * 16 + 8 + p;
       if (*slot == 0) {
         unsigned long long tt;
@@ -928,8 +923,8 @@ __device__ __forceinline__ void aux_drain(const PipeArgs& a, PipeSmem& S, const 
     if (k3) k3_bulk_issue(a, x.slot, p, r, x.lane, x.kbuf + nb * kK3Bytes, &x.kbar[nb]);
     if (pend_k >= 0) {   // the one call site of the K3 compute
       k3_bulk_finish(a, x.slot, x.mtb, x.excl, S.th, x.yt, x.ytl, pend_k, pend_r, x.lane, x.kbuf + pend_b * kK3Bytes,
-                     &x.kbar[pend_b], par[pend_b]);
-      par[pend_b] ^= 1u;
+                     &x.kbar[pend_b], (par >> pend_b) & 1u);
+      par ^= 1u << pend_b;
       pend_k = -1;
     }
     if (k3) {
@@ -972,7 +967,15 @@ __device__ __forceinline__ void aux_prologue(const PipeArgs& a, PipeSmem& S, int
   }
   for (int i = at; i < a.n_items * 9; i += n) (&S.scnt[0][0])[i] = 0;
   named_bar(bar, n);
-  if (at == 0) S.sleft = S.pcnt[0];   // queue phase 0 = search tiles
+  if (at == 0) {
+    S.sleft = S.pcnt[0];   // queue phase 0 = search tiles
+    int e = 0;
+    for (int q = 0; q < kAuxPhases; ++q) {
+      S.pdelta[q] = S.plo[q] - e;
+      e += S.pcnt[q];
+      S.pend[q] = e;
+    }
+  }
   // a CTA without search tiles still counts towards every item's completion
   if (S.pcnt[0] == 0 && at < a.n_items) pipe_search_flush(a, a.items[at], S.scnt[at]);
   named_bar(bar, n);
