@@ -295,6 +295,15 @@ def run_ours(args, rank, world, local_rank):
         end.record(stream)
         torch.cuda.nvtx.range_pop()
         torch.cuda.synchronize()
+    if os.environ.get("MTB_PROFILE_RANGE") and graph is not None:
+        # diagnostics: a profiler range of 4 whole steps (ncu --replay-mode
+        # app-range --profile-from-start off) for the DRAM bytes of the real,
+        # concurrent pipeline rather than of one serialised launch
+        torch.cuda.profiler.start()
+        for _ in range(4):
+            graph.replay()
+        torch.cuda.synchronize()
+        torch.cuda.profiler.stop()
     if graph is not None:
         # Events cannot time kernels inside a graph replay: time each K1 launch
         # with events on an instrumented (python-launched) step right after the

@@ -212,8 +212,10 @@ __device__ __forceinline__ void th_word_t(const uint32_t (&g)[8], const ThConst&
   // 40); a funnel shift (nib:acc) >> 4 pushes them in from the top and drops
   // the garbage, so after 8 words word k's flags sit at bits 4k..4k+3.  One
   // FMA-pipe and one ALU-pipe op per word and map.
-  constexpr uint32_t M4 = 0x00204081u << 4;
-  uint32_t m = 0, e = 0;
+  // Two words per funnel shift: the odd word's nibble is gathered 4 bits
+  // higher (magic << 8) and added by the IMAD.HI of the even word.
+  constexpr uint32_t M4 = 0x00204081u << 4, M8 = 0x00204081u << 8;
+  uint32_t m = 0, e = 0, pm = 0, pe = 0;
 #pragma unroll
   for (int k = 0; k < 8; ++k) {
     const uint32_t x = g[k];
@@ -223,8 +225,13 @@ __device__ __forceinline__ void th_word_t(const uint32_t (&g)[8], const ThConst&
     asm("vabsdiff4.u32.u32.u32 %0, %1, %2, %3;" : "=r"(d) : "r"(x), "r"(c.med), "r"(0u));
     const uint32_t sd = (d & L7) + ytl;
     const uint32_t ge = TOL_LO ? ((d | sd) & H) : (((d & yt) | (d & sd) | (yt & sd)) & H);   // |x - med| > tol
-    m = __funnelshift_r(m, __umulhi(gm, M4), 4);
-    e = __funnelshift_r(e, __umulhi(ge, M4), 4);
+    if ((k & 1) == 0) {
+      pm = gm;
+      pe = ge;
+    } else {
+      m = __funnelshift_r(m, __umulhi(pm, M4) + __umulhi(gm, M8), 8);
+      e = __funnelshift_r(e, __umulhi(pe, M4) + __umulhi(ge, M8), 8);
+    }
   }
   const uint32_t keep = valid >= 32 ? 0xffffffffu : (valid <= 0 ? 0u : ((1u << valid) - 1u));
   mw = m & keep;

@@ -10,6 +10,7 @@ profiles/<tag>_ncu.md with the launch list shares and the full-set metrics.
 """
 
 import argparse
+import io
 import collections
 import csv
 import json
@@ -59,6 +60,23 @@ def launch_list(path):
     return agg, len(rows)
 
 
+def stalls(rep):
+    out = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+    r = list(csv.reader(io.StringIO(out)))
+    if len(r) < 3:
+        return {}
+    d = dict(zip(r[0], r[2]))
+    pre = "smsp__pcsamp_warps_issue_stalled_"
+    res = {}
+    for k, v in d.items():
+        if k.startswith(pre) and not k.endswith("not_issued"):
+            try:
+                res[k[len(pre):]] = float(v.replace(",", ""))
+            except ValueError:
+                pass
+    return res
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--full", required=True)
@@ -97,6 +115,13 @@ def main():
             sp=d["sm__throughput.avg.pct_of_peak_sustained_elapsed"],
             wa=d["sm__warps_active.avg.pct_of_peak_sustained_active"],
             ia=d["smsp__issue_active.avg.pct_of_peak_sustained_active"], ins=d["smsp__inst_executed.sum"]))
+    st = stalls(a.full)
+    if st:
+        lines += ["", "## warp-state samples (first captured launch; % of samples)", "",
+                  "| reason | % |", "|---|---:|"]
+        tot = sum(st.values())
+        for k, v in sorted(st.items(), key=lambda kv: -kv[1])[:10]:
+            lines.append(f"| {k} | {100 * v / tot:.1f} |")
     if a.launches:
         agg, n = launch_list(a.launches)
         tot = sum(v[1] for v in agg.values())
