@@ -444,7 +444,7 @@ __device__ __forceinline__ void k3_bulk_units(const PipeArgs& a, uint32_t* mtb, 
   const int nw = a.nw32[K], lh = a.g.lh[K], lw = a.g.lw[K];
   const int boff = (int)a.bit_off32[K];
   const int f0 = kK3Words * r;
-#pragma unroll
+#pragma unroll 1
   for (int i = 0; i < kK3Units; ++i) {
     const int w = i * 32 + lane;
     const int f = f0 + w;
@@ -480,7 +480,7 @@ __device__ __forceinline__ void k3_bulk_units_l0(const PipeArgs& a, uint32_t* mt
   const bool ok = j < nw;
   uint32_t* pm = mtb + (int)a.bit_off32[0] + y0 * nw + j;
   uint32_t* pe = excl + (int)a.bit_off32[0] + y0 * nw + j;
-#pragma unroll
+#pragma unroll 1
   for (int i = 0; i < kK3Units; ++i) {
     const uint4 v0 = *reinterpret_cast<const uint4*>(buf + (i * 32 + lane) * 32);
     const uint4 v1 = *reinterpret_cast<const uint4*>(buf + (i * 32 + lane) * 32 + 16);
