@@ -161,6 +161,29 @@ __device__ __forceinline__ void spin_geq(const uint32_t* p, uint32_t v) {
   while (ld_acquire(p) < v) __nanosleep(100);
 }
 
+// Diagnostics (MTB_PIPE_TRACE): kTraceWords u64 per (launch, CTA).
+//  0..7 stamps, 8+p first task of aux phase p, 16 %smid, 17 entry, 18 exit,
+//  19/20/22 ns spun on search / threshold / gray-slot dependencies,
+//  21 first K1 tile ready, 24+w end of warp w's aux drain.
+constexpr int kTraceWords = 48;
+__device__ __forceinline__ unsigned long long gtime() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+__device__ __forceinline__ void spin_geq_traced(unsigned long long* trace, int slot, const uint32_t* p, uint32_t v) {
+  if (!trace) {
+    spin_geq(p, v);
+    return;
+  }
+  const unsigned long long t0 = gtime();
+  spin_geq(p, v);
+  atomicAdd(trace + slot, gtime() - t0);
+}
+__device__ __forceinline__ unsigned long long* trace_rec(const PipeArgs& a) {
+  return a.trace ? a.trace + ((int64_t)a.j * gridDim.x + blockIdx.x) * kTraceWords : nullptr;
+}
+
 // Lower median of one level's spread histogram (threshold.py:31-39): the
 // smallest m with cumsum[m] >= (total + 1) / 2.  One warp; lane owns 8 bins.
 __device__ __forceinline__ int warp_median(const uint32_t* spread, int lane) {
@@ -597,10 +620,10 @@ __device__ __forceinline__ void pipe_search_tile(const PipeArgs& a, const PipeIt
   const int n = a.n;
   if (lane == 0) {
     if (k + 1 < n) {
-      spin_geq(a.decided + (int64_t)it.pair * n + (k + 1), 1u);
+      spin_geq_traced(trace_rec(a), 19, a.decided + (int64_t)it.pair * n + (k + 1), 1u);
     } else {
-      spin_geq(a.k3_done + it.ref, gridDim.x);
-      spin_geq(a.k3_done + it.tgt, gridDim.x);
+      spin_geq_traced(trace_rec(a), 19, a.k3_done + it.ref, gridDim.x);
+      spin_geq_traced(trace_rec(a), 19, a.k3_done + it.tgt, gridDim.x);
     }
   }
   __syncwarp();
@@ -861,7 +884,7 @@ __device__ __forceinline__ void aux_stamp(const PipeArgs& a, int i) {
   if (a.trace) {
     unsigned long long t;
     asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
-    a.trace[((int64_t)a.j * gridDim.x + blockIdx.x) * 16 + i] = t;
+    a.trace[((int64_t)a.j * gridDim.x + blockIdx.x) * kTraceWords + i] = t;
   }
 }
 
@@ -876,7 +899,7 @@ __device__ __forceinline__ void aux_need_thresholds(const PipeArgs& a, PipeSmem&
   if (lane == 0) claim = atomicCAS(&S.th_state, 0, 1) == 0;
   claim = __shfl_sync(0xffffffffu, claim, 0);
   if (claim) {
-    if (lane == 0) spin_geq(a.med_ready + a.th_img, 1u);
+    if (lane == 0) spin_geq_traced(trace_rec(a), 20, a.med_ready + a.th_img, 1u);
     __syncwarp();
     if (lane < a.n) {
       const int med = __ldcg(a.medians + a.th_img * a.n + lane);
@@ -918,7 +941,7 @@ __device__ __forceinline__ void aux_drain(const PipeArgs& a, PipeSmem& S, const 
     const int p = q < kAuxPhases ? aux_phase_of(a, q) : -1;
     const int r = q < kAuxPhases ? t + S.pdelta[q] : 0;
     if (a.trace && p >= 0 && x.tracer && x.lane == 0) {
-      unsigned long long* slot = a.trace + ((int64_t)a.j * gridDim.x + blockIdx.x) * 16 + 8 + p;
+      unsigned long long* slot = a.trace + ((int64_t)a.j * gridDim.x + blockIdx.x) * kTraceWords + 8 + p;
       if (*slot == 0) {
         unsigned long long tt;
         asm volatile("mov.u64 %0, %globaltimer;" : "=l"(tt));
@@ -996,6 +1019,15 @@ __global__ void __launch_bounds__(kPipeThreads, 1) pipe_kernel(const __grid_cons
   const int tid = threadIdx.x;
   const int lane = tid & 31;
   const int warp = tid >> 5;
+  if (a.trace && threadIdx.x == 0) {   // diagnostics: SM and entry time of this CTA
+    unsigned long long t;
+    uint32_t sm;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+    asm volatile("mov.u32 %0, %smid;" : "=r"(sm));
+    unsigned long long* tr = a.trace + ((int64_t)a.j * gridDim.x + blockIdx.x) * kTraceWords;
+    tr[16] = sm;
+    tr[17] = t;
+  }
   // All dependencies on earlier launches are explicit flags, so the next
   // launch may be scheduled as soon as this one's CTAs are all resident.
   grid_dep_launch();
@@ -1009,7 +1041,7 @@ __global__ void __launch_bounds__(kPipeThreads, 1) pipe_kernel(const __grid_cons
     if (a.trace && (tid == 0 || tid == 32 * kPK1Warps)) {
       unsigned long long t;
       asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
-      a.trace[((int64_t)a.j * gridDim.x + blockIdx.x) * 16 + i] = t;
+      a.trace[((int64_t)a.j * gridDim.x + blockIdx.x) * kTraceWords + i] = t;
     }
   };
 
@@ -1034,8 +1066,10 @@ __global__ void __launch_bounds__(kPipeThreads, 1) pipe_kernel(const __grid_cons
       // Claim the next tile of the image for ring stage `stage` (launch-wide
       // counter: CTAs that start late take fewer tiles) and start its copy;
       // past the end, complete the stage's phase with tile -1.
-      auto claim = [&](int stage) {
-        int tile = (int)atomicAdd(ctr, 1u);
+      // The first tile of each group is static (no atomic round trip before
+      // the CTA's first copy); the counter hands out tiles after those.
+      auto claim = [&](int stage, int fixed) {
+        int tile = fixed >= 0 ? fixed : kPK1Groups * (int)gridDim.x + (int)atomicAdd(ctr, 1u);
         if (tile >= tiles_img) tile = -1;
         S.tile_of[g][stage] = tile;
         if (tile >= 0) {
@@ -1050,11 +1084,13 @@ __global__ void __launch_bounds__(kPipeThreads, 1) pipe_kernel(const __grid_cons
       if (t == 0) {
         for (int s = 0; s < kPStages; ++s) mbar_init(&S.full[g][s], 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-        for (int s = 0; s < kPStages; ++s) claim(s);
+        claim(0, (int)blockIdx.x * kPK1Groups + g);
+        for (int s = 1; s < kPStages; ++s) claim(s, -1);
       }
       // gray slot k1_img % 3 last held image k1_img - 3: wait until every CTA
       // has thresholded it
-      if (kt == 0 && a.k1_img >= kPGraySlots) spin_geq(a.k3_done + (a.k1_img - kPGraySlots), gridDim.x);
+      if (kt == 0 && a.k1_img >= kPGraySlots)
+        spin_geq_traced(trace_rec(a), 22, a.k3_done + (a.k1_img - kPGraySlots), gridDim.x);
       named_bar(5, 32 * kPK1Warps);   // hist zeroed, mbarriers initialised, slot free
       uint8_t* slot = a.g.gray + (int64_t)(a.k1_img % kPGraySlots) * a.g.gray_img_stride;
       int k = 0, ptx = 0, pty = 0, ptile = 0;
@@ -1062,6 +1098,7 @@ __global__ void __launch_bounds__(kPipeThreads, 1) pipe_kernel(const __grid_cons
       for (;; ++k) {
         const int stage = k % kPStages;
         mbar_wait(&S.full[g][stage], (uint32_t)(k / kPStages) & 1u);
+        if (k == 0 && t == 0 && g == 0 && a.trace) trace_rec(a)[21] = gtime();
         const int tile = *reinterpret_cast<volatile int*>(&S.tile_of[g][stage]);
         if (tile < 0) break;
         const int ty = div_tiles_x(a, tile), tx = tile - ty * a.g.tiles_x;
@@ -1077,7 +1114,7 @@ __global__ void __launch_bounds__(kPipeThreads, 1) pipe_kernel(const __grid_cons
         group_bar(g);
         if (t == 0) {
           asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-          claim(stage);
+          claim(stage, -1);
         }
         if (k > 0 && a.g.nl >= 5 && wg == ((k - 1) & 3))
           k1_levels45_tm(a.g, slot + (int64_t)ptile * kTileGrayBytes, S.l3[g][(k - 1) & 1], ptx, pty, lane, hb,
@@ -1169,11 +1206,14 @@ __global__ void __launch_bounds__(kPipeThreads, 1) pipe_kernel(const __grid_cons
   ax.tracer = true;
   if (a.probe != 2) aux_drain(a, S, ax);
   stamp(warp < kPK1Warps ? 3 : 5);
+  if (a.trace && lane == 0) trace_rec(a)[24 + warp] = gtime();
   named_bar(10, kPipeThreads);   // every task of this CTA done
   if (tid == 0 && a.th_img >= 0) {
     __threadfence();
     atomicAdd(a.k3_done + a.th_img, 1u);
   }
+  if (a.trace && tid == 0) trace_rec(a)[18] = gtime();
+
 }
 
 bool k1_rgb_supported(int w, int64_t rgb_pitch, int64_t rgb_img_stride, const void* rgb);
