@@ -164,8 +164,9 @@ __device__ __forceinline__ void spin_geq(const uint32_t* p, uint32_t v) {
 // Diagnostics (MTB_PIPE_TRACE): kTraceWords u64 per (launch, CTA).
 //  0..7 stamps, 8+p first task of aux phase p, 16 %smid, 17 entry, 18 exit,
 //  19/20/22 ns spun on search / threshold / gray-slot dependencies,
-//  21 first K1 tile ready, 24+w end of warp w's aux drain.
-constexpr int kTraceWords = 48;
+//  21 first K1 tile ready, 24+w end of warp w's aux drain, 40+w / 56+w start
+//  and phase of the last task warp w claimed.
+constexpr int kTraceWords = 80;
 __device__ __forceinline__ unsigned long long gtime() {
   unsigned long long t;
   asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
@@ -940,6 +941,10 @@ __device__ __forceinline__ void aux_drain(const PipeArgs& a, PipeSmem& S, const 
     while (q < kAuxPhases && t >= S.pend[q]) ++q;
     const int p = q < kAuxPhases ? aux_phase_of(a, q) : -1;
     const int r = q < kAuxPhases ? t + S.pdelta[q] : 0;
+    if (a.trace && p >= 0 && x.lane == 0) {   // last task claimed by this warp: start, phase
+      trace_rec(a)[40 + (threadIdx.x >> 5)] = gtime();
+      trace_rec(a)[56 + (threadIdx.x >> 5)] = p;
+    }
     if (a.trace && p >= 0 && x.tracer && x.lane == 0) {
       unsigned long long* slot = a.trace + ((int64_t)a.j * gridDim.x + blockIdx.x) * kTraceWords + 8 + p;
       if (*slot == 0) {

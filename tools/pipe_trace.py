@@ -14,7 +14,7 @@ pairs = [(2 * p, 2 * p + 1) for p in range(P)]
 pyr = eng.alloc(2 * P)
 J = 2 * P + 1 + eng.n
 G = torch.cuda.get_device_properties(0).multi_processor_count
-tr = torch.zeros(J * G * 48, dtype=torch.int64, device="cuda")
+tr = torch.zeros(J * G * 80, dtype=torch.int64, device="cuda")
 for it in range(4):
     if it == 3:
         os.environ["MTB_PIPE_TRACE"] = str(tr.data_ptr())
@@ -24,7 +24,7 @@ for it in range(4):
     e.record()
     torch.cuda.synchronize()
     print("step ms", s.elapsed_time(e))
-t = tr.view(J, G, 48).cpu().numpy().astype(np.int64)
+t = tr.view(J, G, 80).cpu().numpy().astype(np.int64)
 t0 = t[0, :, 0].min()
 print("launch  k1_start(min,max) k1_tiles flush k1_aux k1_end_max | aux_start(min,max) aux  aux_end_max   (us; medians over CTAs)")
 for j in range(J):

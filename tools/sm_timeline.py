@@ -16,7 +16,7 @@ pairs = [(2 * p, 2 * p + 1) for p in range(P)]
 pyr = eng.alloc(2 * P)
 J = 2 * P + 1 + eng.n
 G = torch.cuda.get_device_properties(0).multi_processor_count
-tr = torch.zeros(J * G * 48, dtype=torch.int64, device="cuda")
+tr = torch.zeros(J * G * 80, dtype=torch.int64, device="cuda")
 for it in range(4):
     if it == 3:
         os.environ["MTB_PIPE_TRACE"] = str(tr.data_ptr())
@@ -26,7 +26,7 @@ for it in range(4):
     e.record()
     torch.cuda.synchronize()
     print("step ms", s.elapsed_time(e))
-t = tr.view(J, G, 48).cpu().numpy().astype(np.int64)
+t = tr.view(J, G, 80).cpu().numpy().astype(np.int64)
 sm, t_in, t_out = t[:, :, 16], t[:, :, 17], t[:, :, 18]
 t0 = t_in.min()
 span = (t_out.max() - t0) / 1e3
@@ -59,3 +59,19 @@ print("spin ns per CTA: search deps %.0f  thresholds %.0f  gray slot %.0f" % tup
 wmax = we.max(axis=2)
 print("exit - last warp end us: median %.2f p90 %.2f" % (np.median((t_out[mid] - wmax[mid]) / 1e3), np.percentile((t_out[mid] - wmax[mid]) / 1e3, 90)))
 print("last warp end - first warp end us: median %.2f" % np.median((wmax[mid] - we.min(axis=2)[mid]) / 1e3))
+# the slowest warp of each CTA: its last task's phase and duration
+ls, lp = t[:, :, 40:56], t[:, :, 56:72]
+arg = we.argmax(axis=2)
+import collections
+ph = collections.Counter()
+durs = collections.defaultdict(list)
+for j in range(10, J - 10):
+    for c in range(G):
+        w = arg[j, c]
+        ph[int(lp[j, c, w])] += 1
+        durs[int(lp[j, c, w])].append((we[j, c, w] - ls[j, c, w]) / 1e3)
+names = {6: "search", 0: "K3 L0", 1: "K3 L1", 2: "K3 L2", 3: "K3 L3", 4: "L4-5", 5: "pad"}
+print("slowest warp's last task:", ", ".join(f"{names.get(k, k)} {v} (med {np.median(durs[k]):.2f} us)" for k, v in ph.most_common()))
+# all warps: last task phase distribution and duration
+allp = collections.Counter(lp[10:J - 10].ravel().tolist())
+print("all warps' last task:", ", ".join(f"{names.get(k, k)} {v}" for k, v in allp.most_common()))
