@@ -277,6 +277,23 @@ int mtb_align_fused(const uint8_t* rgb, int64_t rgb_pitch, int64_t rgb_img_strid
                     uint32_t* hist_ws, int32_t* medians, uint64_t* mtb, uint64_t* exclusion, int32_t* acc,
                     unsigned long long* errs, uint32_t* done, uint32_t* sync_ws, void* stream);
 
+/* 5. Ingest (decode_image imageio.py:82-94 -> pinned host ->
+ * H2D overlapped with K1).  mtb_align_fused with streamed input: the RGB
+ * batch may still be arriving; K1 of image i starts once img_ready[i] != 0.
+ * The caller zeroes img_ready before the call (stream-ordered before it) and
+ * sets each flag after that image's H2D copy with mtb_stream_write_u32 on the
+ * copy stream; img_ready = NULL is mtb_align_fused. */
+int mtb_align_fused_ex(const uint8_t* rgb, int64_t rgb_pitch, int64_t rgb_img_stride, int w, int h, int n_img,
+                       int levels, int tol, const int32_t* pairs_host, int n_pairs, uint8_t* gray_ws,
+                       uint32_t* hist_ws, int32_t* medians, uint64_t* mtb, uint64_t* exclusion, int32_t* acc,
+                       unsigned long long* errs, uint32_t* done, uint32_t* sync_ws, const uint32_t* img_ready,
+                       void* stream);
+
+/* Stream-ordered store of `value` to device word dptr (cuStreamWriteValue32
+ * with its implicit memory barrier: every earlier operation of the stream,
+ * e.g. an H2D copy, is visible first). */
+int mtb_stream_write_u32(uint32_t* dptr, uint32_t value, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

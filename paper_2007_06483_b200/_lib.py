@@ -61,6 +61,10 @@ SIGNATURES = {
     "mtb_align_fused": [_c_void_p, _i64, _i64, _i32, _i32, _i32, _i32, _i32, _c_void_p, _i32,
                         _c_void_p, _c_void_p, _c_void_p, _c_void_p, _c_void_p, _c_void_p, _c_void_p, _c_void_p,
                         _c_void_p, _c_void_p],
+    "mtb_align_fused_ex": [_c_void_p, _i64, _i64, _i32, _i32, _i32, _i32, _i32, _c_void_p, _i32,
+                           _c_void_p, _c_void_p, _c_void_p, _c_void_p, _c_void_p, _c_void_p, _c_void_p, _c_void_p,
+                           _c_void_p, _c_void_p, _c_void_p],
+    "mtb_stream_write_u32": [_c_void_p, ctypes.c_uint32, _c_void_p],
 }
 
 # Non-status entry points.

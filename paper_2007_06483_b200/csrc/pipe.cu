@@ -77,6 +77,7 @@ struct PipeArgs {
   uint32_t* ctr;                     // [launch] K1 tile counters (zeroed)
   uint32_t* med_ready;               // [img] 1 once the image's medians (and all its gray) are published
   uint32_t* k3_done;                 // [img] CTAs that finished thresholding the image
+  const uint32_t* img_ready;         // [img] nonzero once the image's RGB is in HBM (streamed input), or null
   uint32_t* decided;                 // [P][n] 1 once the (pair, level) offset is published
   int n_launch;
   int search_first;                  // aux task order (MTB_PIPE_SEARCH_FIRST)
@@ -1087,6 +1088,8 @@ __global__ void __launch_bounds__(kPipeThreads, 1) pipe_kernel(const __grid_cons
         }
       };
       if (t == 0) {
+        // streamed input (mtb_align_fused_ex): the image's H2D copy has landed
+        if (a.img_ready) spin_geq(a.img_ready + a.k1_img, 1u);
         for (int s = 0; s < kPStages; ++s) mbar_init(&S.full[g][s], 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
         claim(0, (int)blockIdx.x * kPK1Groups + g);
@@ -1242,11 +1245,11 @@ extern "C" int mtb_align_fused_workspace(int w, int h, int levels, int64_t* gray
   return p.n <= kPipeMaxLevels ? p.n : -1;
 }
 
-extern "C" int mtb_align_fused(const uint8_t* rgb, int64_t rgb_pitch, int64_t rgb_img_stride, int w, int h,
-                               int n_img, int levels, int tol, const int32_t* pairs_host, int n_pairs,
-                               uint8_t* gray_ws, uint32_t* hist_ws, int32_t* medians, uint64_t* mtb,
-                               uint64_t* exclusion, int32_t* acc, unsigned long long* errs, uint32_t* done,
-                               uint32_t* sync_ws, void* stream) {
+extern "C" int mtb_align_fused_ex(const uint8_t* rgb, int64_t rgb_pitch, int64_t rgb_img_stride, int w, int h,
+                                  int n_img, int levels, int tol, const int32_t* pairs_host, int n_pairs,
+                                  uint8_t* gray_ws, uint32_t* hist_ws, int32_t* medians, uint64_t* mtb,
+                                  uint64_t* exclusion, int32_t* acc, unsigned long long* errs, uint32_t* done,
+                                  uint32_t* sync_ws, const uint32_t* img_ready, void* stream) {
   clear_error();
   MTB_REQUIRE(rgb && gray_ws && hist_ws && medians && mtb && exclusion && sync_ws, "null pointer");
   MTB_REQUIRE(n_pairs == 0 || (pairs_host && acc && errs && done), "null pair buffers");
@@ -1323,6 +1326,7 @@ extern "C" int mtb_align_fused(const uint8_t* rgb, int64_t rgb_pitch, int64_t rg
     a.trace = tr ? reinterpret_cast<unsigned long long*>(strtoull(tr, nullptr, 0)) : nullptr;
   }
   a.ctr = sync_ws;
+  a.img_ready = img_ready;
   a.acc = acc;
   a.errs = errs;
   a.done = done;
@@ -1411,4 +1415,39 @@ extern "C" int mtb_align_fused(const uint8_t* rgb, int64_t rgb_pitch, int64_t rg
     ++launches;
   }
   return check_launch("pipe_kernel", launches);
+}
+
+extern "C" int mtb_align_fused(const uint8_t* rgb, int64_t rgb_pitch, int64_t rgb_img_stride, int w, int h,
+                               int n_img, int levels, int tol, const int32_t* pairs_host, int n_pairs,
+                               uint8_t* gray_ws, uint32_t* hist_ws, int32_t* medians, uint64_t* mtb,
+                               uint64_t* exclusion, int32_t* acc, unsigned long long* errs, uint32_t* done,
+                               uint32_t* sync_ws, void* stream) {
+  return mtb_align_fused_ex(rgb, rgb_pitch, rgb_img_stride, w, h, n_img, levels, tol, pairs_host, n_pairs, gray_ws,
+                            hist_ws, medians, mtb, exclusion, acc, errs, done, sync_ws, nullptr, stream);
+}
+
+// Stream-ordered 32-bit store (cuStreamWriteValue32, with its implicit memory
+// barrier): marks an image's H2D copy complete for mtb_align_fused_ex.
+extern "C" int mtb_stream_write_u32(uint32_t* dptr, uint32_t value, void* stream) {
+  clear_error();
+  MTB_REQUIRE(dptr, "null pointer");
+  using WriteFn = CUresult (*)(CUstream, CUdeviceptr, cuuint32_t, unsigned int);
+  static WriteFn fn = nullptr;
+  if (!fn) {
+    cudaDriverEntryPointQueryResult q;
+    void* p = nullptr;
+    if (cudaGetDriverEntryPoint("cuStreamWriteValue32", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<WriteFn>(p);
+  }
+  if (!fn) {
+    set_error("cuStreamWriteValue32 unavailable");
+    return MTB_ECUDA;
+  }
+  if (fn(reinterpret_cast<CUstream>(as_stream(stream)), reinterpret_cast<CUdeviceptr>(dptr), value, 0) !=
+      CUDA_SUCCESS) {
+    set_error("cuStreamWriteValue32 failed");
+    return MTB_ECUDA;
+  }
+  return MTB_OK;
 }

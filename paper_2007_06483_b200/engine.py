@@ -216,7 +216,7 @@ class MtbEngine:
         return ws
 
     def align_fused(self, rgb, pairs, pyr: PyramidSet | None = None, acc=None, errs=None, done=None,
-                    count: bool = True):
+                    count: bool = True, img_ready=None):
         """Preprocess every image of `rgb` and find_offset every (ref, tgt) pair in ONE
         software-pipelined sequence of launches (csrc/pipe.cu): pipeline.py:80-90
         with search.py:74-95, gray pyramids kept in L2.  Returns (pyr, acc, errs)
@@ -241,16 +241,55 @@ class MtbEngine:
         words = int(_lib.load().mtb_align_fused_sync_words(n_img, P, self.n))
         if sync is None or sync.numel() < words:
             sync = ws["sync"] = t.empty(words, dtype=t.int32, device="cuda")
-        _lib.call("mtb_align_fused", _dev.ptr(rgb), 3 * self.width, 3 * self.width * self.height, self.width,
+        _lib.call("mtb_align_fused_ex", _dev.ptr(rgb), 3 * self.width, 3 * self.width * self.height, self.width,
                   self.height, n_img, self.requested_levels, self.tol, pairs.ctypes.data, P, _dev.ptr(ws["gray"]),
                   _dev.ptr(pyr.hist_ws), _dev.ptr(pyr.medians), _dev.ptr(pyr.mtb), _dev.ptr(pyr.excl),
-                  _dev.ptr(acc), _dev.ptr(errs), _dev.ptr(done), _dev.ptr(sync), _dev.stream())
+                  _dev.ptr(acc), _dev.ptr(errs), _dev.ptr(done), _dev.ptr(sync),
+                  _dev.ptr(img_ready) if img_ready is not None else None, _dev.stream())
         if count:
             counters.bump(PYRAMID_BUILDS, n_img)
             counters.bump(MTB_PYRAMID_BUILDS, n_img)
             counters.bump(FIND_OFFSET_CALLS, P)
             counters.bump(SHIFTED_ERROR_EVALS, 9 * self.n * P)
         return pyr, acc[:P], errs[:P]
+
+    def align_fused_host(self, host, pairs, pyr: PyramidSet | None = None, acc=None, errs=None, done=None,
+                         dev=None, count: bool = True):
+        """align_fused on a HOST batch (pinned uint8 [N, H, W, 3], e.g. from
+        imageio.load_stack): each image is copied H2D on a side stream and
+        flagged with a stream-ordered store; K1 of image i waits for its flag
+        inside the pipeline, so the upload overlaps the alignment of the
+        images before it.  `dev` is the device batch to fill
+        (allocated if None).  Returns (dev, pyr, acc, errs)."""
+        t = self.torch
+        if host.is_cuda or host.dtype != t.uint8 or host.dim() != 4 or tuple(host.shape[1:]) != (
+                self.height, self.width, 3):
+            raise ValueError(f"host batch must be a CPU uint8 (N, {self.height}, {self.width}, 3) tensor")
+        n_img = int(host.shape[0])
+        ws = self.fused_workspace()
+        if dev is None:
+            dev = t.empty(tuple(host.shape), dtype=t.uint8, device="cuda")
+        ready = ws.get("ready")
+        if ready is None or ready.numel() < n_img:
+            ready = ws["ready"] = t.empty(max(n_img, 8), dtype=t.int32, device="cuda")
+        cs = ws.get("copy_stream")
+        if cs is None:
+            cs = ws["copy_stream"] = t.cuda.Stream()
+        cur = t.cuda.current_stream()
+        cs.wait_stream(cur)            # dev / ready no longer in use by earlier work
+        with t.cuda.stream(cs):
+            ready[:n_img].zero_()
+        zeroed = t.cuda.Event()
+        zeroed.record(cs)
+        cur.wait_event(zeroed)         # the pipeline never sees a stale flag
+        for i in range(n_img):
+            with t.cuda.stream(cs):
+                dev[i].copy_(host[i], non_blocking=True)
+            _lib.call("mtb_stream_write_u32", _dev.ptr(ready[i]), 1, cs.cuda_stream)
+        dev.record_stream(cs)
+        pyr, acc, errs = self.align_fused(dev, pairs, pyr, acc, errs, done, count=count, img_ready=ready)
+        cur.wait_stream(cs)
+        return dev, pyr, acc, errs
 
     def search(self, pyr: PyramidSet, pairs, count: bool = True):
         table = self.maps_table(pyr, pairs)

@@ -215,6 +215,69 @@ def get_exp_shift(ref_rgb, tgt_rgb, levels: int = DEFAULT_LEVELS, tol: int = DEF
     return ShiftOffset(int(a[0]), int(a[1]))
 
 
+def align_files(paths, levels: int = DEFAULT_LEVELS, tol: int = DEFAULT_NOISE_TOLERANCE, mode: str = "chain",
+                pivot: int | None = None, workers: int | None = None):
+    """Ingest path: decode the files (PPM / PNG, imageio.py:82-94)
+    with a thread pool straight into one pinned batch, upload it image by
+    image on a copy stream overlapped with the fused pipeline (K1 of image i
+    starts when its copy lands), then shift every image onto the anchor.
+
+    Same pairing and re-basing as `align` (chain: onto image 0; pivot: onto
+    the pivot).  Returns (aligned numpy images, StackAlignment) with timings
+    "decode" (host decode), "align" (upload + preprocess + search + readback)
+    and "shift" (shift_rgb + download).
+    """
+    from .imageio import load_stack
+
+    paths = list(paths)
+    n = len(paths)
+    if n < 2:
+        raise ValueError(f"alignment needs at least 2 images; got {n}")
+    if mode == "chain":
+        pairs, anchor = [(i, i + 1) for i in range(n - 1)], None
+    elif mode == "pivot":
+        anchor = n // 2 if pivot is None else int(pivot)
+        if not 0 <= anchor < n:
+            raise ValueError(f"pivot {anchor} out of range for {n} images")
+        pairs = [(anchor, i) for i in range(n) if i != anchor]
+    else:
+        raise ValueError(f"mode must be 'chain' or 'pivot', got {mode!r}")
+    t0 = time.perf_counter()
+    host = load_stack(paths, workers=workers, pinned=True)
+    t1 = time.perf_counter()
+    h, w = int(host.shape[1]), int(host.shape[2])
+    if w < MIN_LEVEL_SIZE or h < MIN_LEVEL_SIZE:
+        raise ValueError(f"images must be at least 16x16; got {w}x{h}")
+    eng = engine_for(w, h, levels, tol)
+    if eng.fused_supported:
+        batch, _, acc, errs = eng.align_fused_host(host, pairs)
+    else:
+        batch = host.to("cuda", non_blocking=True)
+        pyr = eng.preprocess(batch)
+        acc, errs = eng.search(pyr, pairs)
+    pairwise = results_from_device(acc, errs)
+    t2 = time.perf_counter()
+    cumulative = [ShiftOffset(0, 0)] * n
+    if anchor is None:
+        for i, res in enumerate(pairwise, start=1):
+            cumulative[i] = cumulative[i - 1] + res.offset
+    else:
+        for (_, tgt), res in zip(pairs, pairwise):
+            cumulative[tgt] = res.offset
+    keep = 0 if anchor is None else anchor
+    movers = [i for i in range(n) if i != keep]
+    torch = _dev.torch_mod()
+    idx = torch.tensor(movers, dtype=torch.long, device="cuda")
+    shifted = shift_rgb_device(batch.index_select(0, idx).contiguous(), [cumulative[i] for i in movers]).cpu().numpy()
+    hv = host.numpy()
+    aligned = [hv[keep].copy() if i == keep else None for i in range(n)]
+    for j, i in enumerate(movers):
+        aligned[i] = shifted[j]
+    t3 = time.perf_counter()
+    timings = {"decode": (t1 - t0) * 1000.0, "align": (t2 - t1) * 1000.0, "shift": (t3 - t2) * 1000.0}
+    return aligned, StackAlignment(image_count=n, pairwise=pairwise, cumulative=cumulative, timings=timings)
+
+
 def measure_alignment(images: list, repetitions: int = 10, levels: int = DEFAULT_LEVELS,
                       tol: int = DEFAULT_NOISE_TOLERANCE, layout: str = PACKED,
                       workers: int | None = None) -> TimingReport:
