@@ -228,7 +228,7 @@ def run_ours(args, rank, world, local_rank):
     stream = torch.cuda.current_stream()
 
     fused = args.mode == "fused"
-    n_launch_fused = n_img + 1 + eng.n  # pipe.cu: one launch per image + drain (pairs (2p, 2p+1))
+    n_launch_fused = eng.fused_launches(n_img, pairs) if args.mode == "fused" else 0  # pipe.cu launches per step
 
     def step(ev=None):
         if fused:
@@ -361,7 +361,7 @@ def run_ours(args, rank, world, local_rank):
                    "correct_offsets": f"{correct}/{P} match ground truth"},
         "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
                      "frac": round(achieved / peak, 4), "traffic": traffic, "peak_source": peak_src,
-                     "kernel": ("pipe_kernel (fused K1+K3+K4, one launch per image, "
+                     "kernel": ("pipe_kernel (fused K1+K3+K4, two images per launch, "
                                 f"{n_launch_fused} PDL launches per step)") if fused else
                                f"k1_rgb_pyramid_kernel (K1: RGB->gray->pyramid->histograms, {k1_images} images/launch)",
                      "algorithmic_bytes_per_launch": k1_bytes, "avg_launch_ms": round(k1_avg_s * 1e3, 4),

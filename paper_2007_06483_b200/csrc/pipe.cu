@@ -22,6 +22,7 @@
 //      complete after step 2)
 // HBM traffic per image is the RGB read plus the packed maps; the gray
 // round trip (32 MB per 24 MP image) stays in L2.
+#include <algorithm>
 #include <cstdlib>
 #include <cstring>
 #include <type_traits>
@@ -83,8 +84,8 @@ struct PipeArgs {
   int search_first;                  // aux task order (MTB_PIPE_SEARCH_FIRST)
   int probe;                         // diagnostics (MTB_PIPE_PROBE): 1 = no K1 tiles, 2 = no aux tasks
   int j;                             // this launch's index
-  int k1_img;                        // image of the K1 part, or -1
-  int th_img;                        // image of the K3 part, or -1
+  int k1_img0, k1_cnt;               // images k1_img0 .. +k1_cnt-1 of the K1 part (k1_cnt may be 0)
+  int th_img0, th_cnt;               // images of the K3 part
   int n_items;
   int search_tiles;
   unsigned long long* trace;         // optional [launch][cta][8] %globaltimer stamps (diagnostics)                  // total search warp-tiles of this launch
@@ -112,7 +113,11 @@ constexpr int kPK1Groups = PIPE_K1_GROUPS;
 constexpr int kPK1Warps = 4 * kPK1Groups;
 constexpr int kPAuxWarps = kPipeWarps - kPK1Warps;
 constexpr int kPStages = PIPE_STAGES;
-constexpr int kPGraySlots = 3;
+#ifndef PIPE_IMGS
+#define PIPE_IMGS 2
+#endif
+constexpr int kPipeImgs = PIPE_IMGS;          // images per launch (K1 part and K3 part)
+constexpr int kPGraySlots = 3 * kPipeImgs;    // gray ring: written, being read, lagging readers
 constexpr int kAuxPhases = 7;     // aux task phases: K3 levels 0..3, levels 4..5, padding, search
 
 // Per-aux-warp staging of one search warp-tile: 8 output rows x 32 words of
@@ -123,14 +128,15 @@ struct SearchStage {
 };
 
 struct PipeSmem {
-  uint32_t hist[6][256];                                  // 1 KB-aligned levels (see k1_tile.cuh)
+  uint32_t hist[kPipeImgs][6][256];                       // per K1 image; 1 KB-aligned levels (k1_tile.cuh)
   uint8_t rgb[kPK1Groups][kPStages][kK1TileBytes];
   uint8_t abuf[kPAuxWarps > 0 ? kPAuxWarps : 1][2][kK3Bytes];                  // aux warps: K3 double buffer / search staging
   uint8_t l3[kPK1Groups][2][4][32];
   unsigned long long full[kPK1Groups][kPStages];
   int tile_of[kPK1Groups][kPStages];                      // tile in each ring stage (-1: no more)
   unsigned long long kbar[kPipeWarps][2];                 // per-warp K3 staging mbarriers
-  ThConst th[kPipeMaxLevels];
+  ThConst th[kPipeImgs][kPipeMaxLevels];                 // threshold constants of the K3 images
+  int pt1[kAuxPhases];                                    // one image's task count per aux phase
   int last;
   int next;                                               // aux task queue head
   int plo[kAuxPhases], pcnt[kAuxPhases];                  // this CTA's slice of each aux phase
@@ -796,9 +802,6 @@ static_assert(sizeof(SearchStage) <= 2 * kK3Bytes, "search staging fits a warp's
 static_assert(kPStages * kK1TileBytes >= 4 * 12288, "K1 warps stage in their group ring");
 
 struct AuxCtx {
-  const uint8_t* slot;
-  uint32_t* mtb;
-  uint32_t* excl;
   uint32_t yt, ytl;
   int lane;
   SearchStage* stage;          // search staging (aliases kbuf)
@@ -810,8 +813,8 @@ struct AuxCtx {
 __device__ __forceinline__ void named_bar(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory"); }
 
 // Global task count of phase p.
-__device__ __forceinline__ int aux_phase_tasks(const PipeArgs& a, int p) {
-  const bool th = a.th_img >= 0;
+__device__ __forceinline__ int aux_phase_tasks1(const PipeArgs& a, int p) {
+  const bool th = a.th_cnt > 0;
   switch (p) {
     case 0: return th ? (th_level_units<0>(a) + kK3Units - 1) / kK3Units : 0;
     case 1: return th && a.n > 1 ? (th_level_units<1>(a) + kK3Units - 1) / kK3Units : 0;
@@ -822,9 +825,22 @@ __device__ __forceinline__ int aux_phase_tasks(const PipeArgs& a, int p) {
     default: return a.search_tiles;   // 6
   }
 }
+// K3 / level 4-5 / padding phases hold th_cnt images' tasks back to back.
+__device__ __forceinline__ int aux_phase_tasks(const PipeArgs& a, int p) {
+  return p < 6 ? a.th_cnt * aux_phase_tasks1(a, p) : a.search_tiles;
+}
+__device__ __forceinline__ const uint8_t* aux_slot(const PipeArgs& a, int b) {
+  return a.g.gray + (int64_t)((a.th_img0 + b) % kPGraySlots) * a.g.gray_img_stride;
+}
+__device__ __forceinline__ uint32_t* aux_mtb(const PipeArgs& a, int b) {
+  return a.mtb + (int64_t)(a.th_img0 + b) * a.bit_img_words32;
+}
+__device__ __forceinline__ uint32_t* aux_excl(const PipeArgs& a, int b) {
+  return a.excl + (int64_t)(a.th_img0 + b) * a.bit_img_words32;
+}
 
 // Zero padding words: flat index f over levels 0..3 of (row, uncovered word).
-__device__ __forceinline__ void aux_pad(const PipeArgs& a, const AuxCtx& x, int f) {
+__device__ __forceinline__ void aux_pad(const PipeArgs& a, uint32_t* mtb, uint32_t* excl, int f) {
 #pragma unroll
   for (int k = 0; k < 4; ++k) {
     if (k >= a.n) return;
@@ -835,8 +851,8 @@ __device__ __forceinline__ void aux_pad(const PipeArgs& a, const AuxCtx& x, int 
     if (f < cnt) {
       const int y = f / npad, j = j0 + (f - y * npad);
       const int64_t o = a.bit_off32[k] + (int64_t)y * a.nw32[k] + j;
-      x.mtb[o] = 0u;
-      x.excl[o] = 0u;
+      mtb[o] = 0u;
+      excl[o] = 0u;
       return;
     }
     f -= cnt;
@@ -844,21 +860,22 @@ __device__ __forceinline__ void aux_pad(const PipeArgs& a, const AuxCtx& x, int 
 }
 
 // Runs global task `t` of phase `p`.
-__device__ __forceinline__ void aux_run(const PipeArgs& a, PipeSmem& S, const AuxCtx& x, int p, int t) {
+__device__ __forceinline__ void aux_run(const PipeArgs& a, PipeSmem& S, const AuxCtx& x, int p, int t, int b) {
   switch (p) {
     case 4: {
-      const ThUnit r = th_unit(a, x.slot, a.th_units0[a.n < 4 ? a.n : 4] + t, x.lane);
+      const uint8_t* slot = aux_slot(a, b);
+      const ThUnit r = th_unit(a, slot, a.th_units0[a.n < 4 ? a.n : 4] + t, x.lane);
       uint32_t g8[8];
-      if (r.k == 4) th_gather45<4>(a, x.slot, r, g8);
-      else th_gather45<5>(a, x.slot, r, g8);
+      if (r.k == 4) th_gather45<4>(a, slot, r, g8);
+      else th_gather45<5>(a, slot, r, g8);
       uint32_t m, e;
-      th_word(g8, S.th[r.k], x.yt, x.ytl, r.valid, m, e);
-      if (r.out >= 0) { x.mtb[r.out] = m; x.excl[r.out] = e; }
+      th_word(g8, S.th[b][r.k], x.yt, x.ytl, r.valid, m, e);
+      if (r.out >= 0) { aux_mtb(a, b)[r.out] = m; aux_excl(a, b)[r.out] = e; }
       break;
     }
     case 5: {
       const int f = t * 32 + x.lane;
-      if (f < a.th_pad_words) aux_pad(a, x, f);
+      if (f < a.th_pad_words) aux_pad(a, aux_mtb(a, b), aux_excl(a, b), f);
       break;
     }
     default: {
@@ -901,16 +918,17 @@ __device__ __forceinline__ void aux_need_thresholds(const PipeArgs& a, PipeSmem&
   if (lane == 0) claim = atomicCAS(&S.th_state, 0, 1) == 0;
   claim = __shfl_sync(0xffffffffu, claim, 0);
   if (claim) {
-    if (lane == 0) spin_geq_traced(trace_rec(a), 20, a.med_ready + a.th_img, 1u);
+    if (lane < a.th_cnt) spin_geq_traced(trace_rec(a), 20, a.med_ready + a.th_img0 + lane, 1u);
     __syncwarp();
-    if (lane < a.n) {
-      const int med = __ldcg(a.medians + a.th_img * a.n + lane);
+    if (lane < a.n * a.th_cnt) {
+      const int b = lane / a.n, k = lane - b * a.n;
+      const int med = __ldcg(a.medians + (a.th_img0 + b) * a.n + k);
       ThConst c;
       c.med = (uint32_t)med * 0x01010101u;
       c.ym = (uint32_t)(255 - med) * 0x01010101u;
       c.yml = c.ym & 0x7f7f7f7fu;
       c.med_lo = med <= 127;
-      S.th[lane] = c;
+      S.th[b][k] = c;
     }
     __threadfence_block();
     __syncwarp();
@@ -932,7 +950,8 @@ __device__ __forceinline__ void aux_drain(const PipeArgs& a, PipeSmem& S, const 
   }
   __syncwarp();
   uint32_t par = 0u;                         // mbarrier phase bit per staging buffer
-  int pend_k = -1, pend_r = 0, pend_b = 0;   // K3 task in flight
+  int pend_k = -1, pend_r = 0, pend_b = 0;   // K3 task in flight (level, task, staging buffer)
+  int pend_img = 0;                          // ... and its image (0 .. th_cnt-1)
   int nb = 0;                                // next staging buffer
   int q = 0;                                 // queue phase (a warp's claims only grow)
   for (;;) {
@@ -941,7 +960,15 @@ __device__ __forceinline__ void aux_drain(const PipeArgs& a, PipeSmem& S, const 
     t = __shfl_sync(0xffffffffu, t, 0);
     while (q < kAuxPhases && t >= S.pend[q]) ++q;
     const int p = q < kAuxPhases ? aux_phase_of(a, q) : -1;
-    const int r = q < kAuxPhases ? t + S.pdelta[q] : 0;
+    int r = q < kAuxPhases ? t + S.pdelta[q] : 0;
+    int bi = 0;   // K3 / level 4-5 / padding tasks: which of the th_cnt images
+    if (p >= 0 && p < 6) {
+      const int t1 = S.pt1[p];
+      while (bi + 1 < kPipeImgs && r >= t1) {
+        r -= t1;
+        ++bi;
+      }
+    }
     if (a.trace && p >= 0 && x.lane == 0) {   // last task claimed by this warp: start, phase
       trace_rec(a)[40 + (threadIdx.x >> 5)] = gtime();
       trace_rec(a)[56 + (threadIdx.x >> 5)] = p;
@@ -956,23 +983,24 @@ __device__ __forceinline__ void aux_drain(const PipeArgs& a, PipeSmem& S, const 
     }
     const bool k3 = p >= 0 && p < 4;
     if (k3) aux_need_thresholds(a, S, x.lane);
-    if (k3) k3_bulk_issue(a, x.slot, p, r, x.lane, x.kbuf + nb * kK3Bytes, &x.kbar[nb]);
+    if (k3) k3_bulk_issue(a, aux_slot(a, bi), p, r, x.lane, x.kbuf + nb * kK3Bytes, &x.kbar[nb]);
     if (pend_k >= 0) {   // the one call site of the K3 compute
-      k3_bulk_finish(a, x.slot, x.mtb, x.excl, S.th, x.yt, x.ytl, pend_k, pend_r, x.lane, x.kbuf + pend_b * kK3Bytes,
-                     &x.kbar[pend_b], (par >> pend_b) & 1u);
+      k3_bulk_finish(a, aux_slot(a, pend_img), aux_mtb(a, pend_img), aux_excl(a, pend_img), S.th[pend_img], x.yt,
+                     x.ytl, pend_k, pend_r, x.lane, x.kbuf + pend_b * kK3Bytes, &x.kbar[pend_b], (par >> pend_b) & 1u);
       par ^= 1u << pend_b;
       pend_k = -1;
     }
     if (k3) {
       pend_k = p;
       pend_r = r;
+      pend_img = bi;
       pend_b = nb;
       nb ^= 1;
       continue;
     }
     if (p < 0) return;
     if (p == 4) aux_need_thresholds(a, S, x.lane);
-    aux_run(a, S, x, p, r);
+    aux_run(a, S, x, p, r, bi);
     if (p == 6) {
       // last search tile of this CTA: publish its partial counts
       __syncwarp();
@@ -998,6 +1026,7 @@ __device__ __forceinline__ void aux_prologue(const PipeArgs& a, PipeSmem& S, int
   if (at < kAuxPhases) {
     const int G = gridDim.x, c = blockIdx.x;
     const int T = aux_phase_tasks(a, aux_phase_of(a, at));
+    S.pt1[aux_phase_of(a, at)] = aux_phase_tasks1(a, aux_phase_of(a, at));
     S.plo[at] = (int)((int64_t)c * T / G);
     S.pcnt[at] = (int)((int64_t)(c + 1) * T / G) - S.plo[at];
   }
@@ -1059,8 +1088,9 @@ __global__ void __launch_bounds__(kPipeThreads, 1) pipe_kernel(const __grid_cons
     const int kt = tid;               // 0..255 among the K1 threads
     const uint32_t hb = smem_addr(&S.hist[0][0]);
     stamp(0);
-    if (a.k1_img >= 0) {
-      const int tiles_img = a.probe == 1 ? 0 : a.g.tiles_x * a.g.tiles_y;   // probe 1: no tiles, still publish
+    if (a.k1_cnt > 0) {
+      const int tiles_img = a.g.tiles_x * a.g.tiles_y;
+      const int tiles_all = a.probe == 1 ? 0 : a.k1_cnt * tiles_img;   // probe 1: no tiles, still publish
       uint32_t* ctr = a.ctr + a.j;   // K1 tile counter of this launch
       uint64_t pol_first;
       asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol_first));
@@ -1068,47 +1098,59 @@ __global__ void __launch_bounds__(kPipeThreads, 1) pipe_kernel(const __grid_cons
       uint64_t gpol;
       asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(gpol));
 #endif
-      for (int i = kt; i < 6 * 256; i += 32 * kPK1Warps) (&S.hist[0][0])[i] = 0;
-      // Claim the next tile of the image for ring stage `stage` (launch-wide
-      // counter: CTAs that start late take fewer tiles) and start its copy;
-      // past the end, complete the stage's phase with tile -1.
-      // The first tile of each group is static (no atomic round trip before
-      // the CTA's first copy); the counter hands out tiles after those.
+      for (int i = kt; i < kPipeImgs * 6 * 256; i += 32 * kPK1Warps) (&S.hist[0][0][0])[i] = 0;
+      // Claim the next tile for ring stage `stage` (launch-wide counter over
+      // the k1_cnt images' tiles, image-major: CTAs that start late take
+      // fewer tiles) and start its copy; past the end, complete the stage's
+      // phase with tile -1.  The first tile of each group is static (no
+      // atomic round trip before the CTA's first copy).
       auto claim = [&](int stage, int fixed) {
         int tile = fixed >= 0 ? fixed : kPK1Groups * (int)gridDim.x + (int)atomicAdd(ctr, 1u);
-        if (tile >= tiles_img) tile = -1;
+        if (tile >= tiles_all) tile = -1;
         S.tile_of[g][stage] = tile;
         if (tile >= 0) {
-          const int ty = div_tiles_x(a, tile), tx = tile - ty * a.g.tiles_x;
+          int b = 0, t1 = tile;
+          while (t1 >= tiles_img) {
+            t1 -= tiles_img;
+            ++b;
+          }
+          const int ty = div_tiles_x(a, t1), tx = t1 - ty * a.g.tiles_x;
           mbar_expect_tx(&S.full[g][stage], kK1TileBytes);
-          tma_tile(S.rgb[g][stage], &rgb_map, (kK1RowBytes / 4) * tx, kK1TileRows * ty, a.k1_img, &S.full[g][stage],
-                   pol_first);
+          tma_tile(S.rgb[g][stage], &rgb_map, (kK1RowBytes / 4) * tx, kK1TileRows * ty, a.k1_img0 + b,
+                   &S.full[g][stage], pol_first);
         } else {
           asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_addr(&S.full[g][stage])) : "memory");
         }
       };
       if (t == 0) {
-        // streamed input (mtb_align_fused_ex): the image's H2D copy has landed
-        if (a.img_ready) spin_geq(a.img_ready + a.k1_img, 1u);
+        // streamed input (mtb_align_fused_ex): the images' H2D copies have landed
+        if (a.img_ready)
+          for (int b = 0; b < a.k1_cnt; ++b) spin_geq(a.img_ready + a.k1_img0 + b, 1u);
         for (int s = 0; s < kPStages; ++s) mbar_init(&S.full[g][s], 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
         claim(0, (int)blockIdx.x * kPK1Groups + g);
         for (int s = 1; s < kPStages; ++s) claim(s, -1);
       }
-      // gray slot k1_img % 3 last held image k1_img - 3: wait until every CTA
-      // has thresholded it
-      if (kt == 0 && a.k1_img >= kPGraySlots)
-        spin_geq_traced(trace_rec(a), 22, a.k3_done + (a.k1_img - kPGraySlots), gridDim.x);
-      named_bar(5, 32 * kPK1Warps);   // hist zeroed, mbarriers initialised, slot free
-      uint8_t* slot = a.g.gray + (int64_t)(a.k1_img % kPGraySlots) * a.g.gray_img_stride;
-      int k = 0, ptx = 0, pty = 0, ptile = 0;
+      // gray slot i % kPGraySlots last held image i - kPGraySlots: wait until
+      // every CTA has thresholded it
+      if (kt < a.k1_cnt && a.k1_img0 + kt >= kPGraySlots)
+        spin_geq_traced(trace_rec(a), 22, a.k3_done + (a.k1_img0 + kt - kPGraySlots), gridDim.x);
+      named_bar(5, 32 * kPK1Warps);   // hist zeroed, mbarriers initialised, slots free
+      int k = 0, ptx = 0, pty = 0;
+      uint8_t* ptg = nullptr;
+      uint32_t phb = hb;
       bool pfull = true;
       for (;; ++k) {
         const int stage = k % kPStages;
         mbar_wait(&S.full[g][stage], (uint32_t)(k / kPStages) & 1u);
         if (k == 0 && t == 0 && g == 0 && a.trace) trace_rec(a)[21] = gtime();
-        const int tile = *reinterpret_cast<volatile int*>(&S.tile_of[g][stage]);
+        int tile = *reinterpret_cast<volatile int*>(&S.tile_of[g][stage]);
         if (tile < 0) break;
+        int b = 0;
+        while (tile >= tiles_img) {
+          tile -= tiles_img;
+          ++b;
+        }
         const int ty = div_tiles_x(a, tile), tx = tile - ty * a.g.tiles_x;
         const bool full = (ty * kK1TileRows + kK1TileRows <= a.g.h) && (tx * kK1TilePx + kK1TilePx <= a.g.w);
         uint2 v[8][3];
@@ -1125,27 +1167,28 @@ __global__ void __launch_bounds__(kPipeThreads, 1) pipe_kernel(const __grid_cons
           claim(stage, -1);
         }
         if (k > 0 && a.g.nl >= 5 && wg == ((k - 1) & 3))
-          k1_levels45_tm(a.g, slot + (int64_t)ptile * kTileGrayBytes, S.l3[g][(k - 1) & 1], ptx, pty, lane, hb,
-                         pfull);
-        uint8_t* tg = slot + (int64_t)tile * kTileGrayBytes;
+          k1_levels45_tm(a.g, ptg, S.l3[g][(k - 1) & 1], ptx, pty, lane, phb, pfull);
+        const int img = a.k1_img0 + b;
+        uint8_t* tg = a.g.gray + (int64_t)(img % kPGraySlots) * a.g.gray_img_stride + (int64_t)tile * kTileGrayBytes;
+        const uint32_t hbi = hb + (uint32_t)b * (6 * 256 * 4);
         uint8_t* l3_slot = &S.l3[g][k & 1][wg][lane];
         if (full)
-          k1_block_tm<true>(a.g, tg, v, tx, ty, wg, lane, hb, l3_slot TM_POLARG);
+          k1_block_tm<true>(a.g, tg, v, tx, ty, wg, lane, hbi, l3_slot TM_POLARG);
         else
-          k1_block_tm<false>(a.g, tg, v, tx, ty, wg, lane, hb, l3_slot TM_POLARG);
+          k1_block_tm<false>(a.g, tg, v, tx, ty, wg, lane, hbi, l3_slot TM_POLARG);
         ptx = tx;
         pty = ty;
-        ptile = tile;
+        ptg = tg;
+        phb = hbi;
         pfull = full;
       }
       group_bar(g);
       if (k > 0 && a.g.nl >= 5 && wg == ((k - 1) & 3))
-        k1_levels45_tm(a.g, slot + (int64_t)ptile * kTileGrayBytes, S.l3[g][(k - 1) & 1], ptx, pty, lane, hb,
-                       pfull);
+        k1_levels45_tm(a.g, ptg, S.l3[g][(k - 1) & 1], ptx, pty, lane, phb, pfull);
       // The last K1 warp of the CTA to finish flushes the CTA's histograms;
-      // if this is the last CTA of image k1_img it also publishes the medians
-      // (threshold.py:31-39).  Counter: word 1 of bin 0's 128-B line.  The
-      // other K1 warps go straight to the aux work.
+      // for each image of which this is the last CTA it also publishes the
+      // medians (threshold.py:31-39).  Counter: word 1 of bin 0's 128-B line.
+      // The other K1 warps go straight to the aux work.
       stamp(1);
       int mine = 0;
       if (lane == 0) {
@@ -1155,26 +1198,29 @@ __global__ void __launch_bounds__(kPipeThreads, 1) pipe_kernel(const __grid_cons
       mine = __shfl_sync(0xffffffffu, mine, 0);
       if (mine) {
         __threadfence_block();
-        uint32_t* gh = a.g.hist + (int64_t)a.k1_img * a.g.hist_img_stride;
-        for (int i = lane; i < a.g.nl * 256; i += 32) {
-          const uint32_t c = *reinterpret_cast<volatile uint32_t*>(&(&S.hist[0][0])[i]);
-          if (c) atomicAdd(&gh[(int64_t)i * kHistStrideK1], c);
-        }
-        int last = 0;
-        if (lane == 0) {
-          __threadfence();
-          last = atomicAdd(gh + 1, 1u) == gridDim.x - 1;
-        }
-        last = __shfl_sync(0xffffffffu, last, 0);
-        if (last) {
-          __threadfence();
-          for (int k = 0; k < a.n; ++k) {
-            const int m = warp_median(gh + k * 256 * kHistStrideK1, lane);
-            if (lane == 0) a.medians[a.k1_img * a.n + k] = m;
+        for (int b = 0; b < a.k1_cnt; ++b) {
+          const int img = a.k1_img0 + b;
+          uint32_t* gh = a.g.hist + (int64_t)img * a.g.hist_img_stride;
+          for (int i = lane; i < a.g.nl * 256; i += 32) {
+            const uint32_t c = *reinterpret_cast<volatile uint32_t*>(&(&S.hist[b][0][0])[i]);
+            if (c) atomicAdd(&gh[(int64_t)i * kHistStrideK1], c);
           }
+          int last = 0;
           if (lane == 0) {
             __threadfence();
-            atomicExch(a.med_ready + a.k1_img, 1u);
+            last = atomicAdd(gh + 1, 1u) == gridDim.x - 1;
+          }
+          last = __shfl_sync(0xffffffffu, last, 0);
+          if (last) {
+            __threadfence();
+            for (int k = 0; k < a.n; ++k) {
+              const int m = warp_median(gh + k * 256 * kHistStrideK1, lane);
+              if (lane == 0) a.medians[img * a.n + k] = m;
+            }
+            if (lane == 0) {
+              __threadfence();
+              atomicExch(a.med_ready + img, 1u);
+            }
           }
         }
         stamp(2);
@@ -1198,9 +1244,6 @@ __global__ void __launch_bounds__(kPipeThreads, 1) pipe_kernel(const __grid_cons
 
   // ============ every warp: this CTA's share of the aux tasks ================
   AuxCtx ax;
-  ax.slot = a.g.gray + (int64_t)((a.th_img >= 0 ? a.th_img : 0) % kPGraySlots) * a.g.gray_img_stride;
-  ax.mtb = a.mtb + (int64_t)(a.th_img >= 0 ? a.th_img : 0) * a.bit_img_words32;
-  ax.excl = a.excl + (int64_t)(a.th_img >= 0 ? a.th_img : 0) * a.bit_img_words32;
   ax.yt = (uint32_t)(255 - a.tol) * 0x01010101u;
   ax.ytl = ax.yt & 0x7f7f7f7fu;
   ax.lane = lane;
@@ -1216,9 +1259,9 @@ __global__ void __launch_bounds__(kPipeThreads, 1) pipe_kernel(const __grid_cons
   stamp(warp < kPK1Warps ? 3 : 5);
   if (a.trace && lane == 0) trace_rec(a)[24 + warp] = gtime();
   named_bar(10, kPipeThreads);   // every task of this CTA done
-  if (tid == 0 && a.th_img >= 0) {
+  if (tid == 0 && a.th_cnt > 0) {
     __threadfence();
-    atomicAdd(a.k3_done + a.th_img, 1u);
+    for (int b = 0; b < a.th_cnt; ++b) atomicAdd(a.k3_done + a.th_img0 + b, 1u);
   }
   if (a.trace && tid == 0) trace_rec(a)[18] = gtime();
 
@@ -1231,6 +1274,8 @@ int64_t spread_hist_elems(int n_levels);
 }  // namespace mtb
 
 using namespace mtb;
+
+extern "C" int mtb_align_fused_images_per_launch() { return kPipeImgs; }
 
 extern "C" int64_t mtb_align_fused_sync_words(int n_img, int n_pairs, int levels) {
   return (int64_t)(n_img + 8) + 2 * (int64_t)n_img + (int64_t)n_pairs * (levels < 1 ? 1 : levels);
@@ -1337,12 +1382,16 @@ extern "C" int mtb_align_fused_ex(const uint8_t* rgb, int64_t rgb_pitch, int64_t
     MTB_CUDA(cudaMemsetAsync(done, 0, sizeof(uint32_t) * p.n * n_pairs, st));
   }
 
-  // Pair q runs level n-1-(j-t(q)) in launch j, t(q) = max(ref, tgt) + 2.
+  // Launch j runs K1 of images jB .. jB+B-1 and K3 of images (j-1)B ..
+  // (B = kPipeImgs); pair q runs level n-1-(j-t(q)) in launch j, t(q) =
+  // max(ref, tgt) / B + 2 (the launch after its images' K3).
+  const int B = kPipeImgs;
+  const int k1_launches = (n_img + B - 1) / B;
   std::vector<int> ready(n_pairs);
-  int J = n_img + 1;
+  int J = k1_launches + 1;
   for (int q = 0; q < n_pairs; ++q) {
     const int r = pairs_host[2 * q], tg = pairs_host[2 * q + 1];
-    ready[q] = (r > tg ? r : tg) + 2;
+    ready[q] = (r > tg ? r : tg) / B + 2;
     if (ready[q] + p.n > J) J = ready[q] + p.n;
   }
   // sync_ws (mtb_align_fused_sync_words): [J] K1 tile counters, [n_img]
@@ -1381,8 +1430,10 @@ extern "C" int mtb_align_fused_ex(const uint8_t* rgb, int64_t rgb_pitch, int64_t
   int launches = 0;
   for (int j = 0; j < J; ++j) {
     a.j = j;
-    a.k1_img = j < n_img ? j : -1;
-    a.th_img = (j >= 1 && j <= n_img) ? j - 1 : -1;
+    a.k1_img0 = j * B;
+    a.k1_cnt = std::max(0, std::min(B, n_img - j * B));
+    a.th_img0 = (j - 1) * B;
+    a.th_cnt = j >= 1 ? std::max(0, std::min(B, n_img - (j - 1) * B)) : 0;
     a.n_items = 0;
     a.search_tiles = 0;
     for (int q = 0; q < n_pairs; ++q) {

@@ -253,6 +253,14 @@ class MtbEngine:
             counters.bump(SHIFTED_ERROR_EVALS, 9 * self.n * P)
         return pyr, acc[:P], errs[:P]
 
+    def fused_launches(self, n_img: int, pairs) -> int:
+        """Launch count of align_fused for n_img images and these pairs."""
+        b = int(_lib.load().mtb_align_fused_images_per_launch())
+        j = -(-int(n_img) // b) + 1
+        for r, t in pairs:
+            j = max(j, max(int(r), int(t)) // b + 2 + self.n)
+        return j
+
     def align_fused_host(self, host, pairs, pyr: PyramidSet | None = None, acc=None, errs=None, done=None,
                          dev=None, count: bool = True):
         """align_fused on a HOST batch (pinned uint8 [N, H, W, 3], e.g. from

@@ -14,7 +14,7 @@ eng = mtb.MtbEngine(W, H, 6, 4)
 batch, truth = make_inputs(torch, eng, P, seed=1)
 pairs = [(2 * p, 2 * p + 1) for p in range(P)]
 pyr = eng.alloc(2 * P)
-J = 2 * P + 1 + eng.n
+J = eng.fused_launches(2 * P, pairs)
 G = torch.cuda.get_device_properties(0).multi_processor_count
 tr = torch.zeros(J * G * 80, dtype=torch.int64, device="cuda")
 for it in range(4):
