@@ -953,22 +953,35 @@ __device__ __forceinline__ void aux_drain(const PipeArgs& a, PipeSmem& S, const 
   int pend_k = -1, pend_r = 0, pend_b = 0;   // K3 task in flight (level, task, staging buffer)
   int pend_img = 0;                          // ... and its image (0 .. th_cnt-1)
   int nb = 0;                                // next staging buffer
-  int q = 0;                                 // queue phase (a warp's claims only grow)
+  // Queue phase of the last claim: a warp's claims only grow, so the phase
+  // bounds are reloaded only when a claim crosses the current phase's end.
+  int q = -1, qend = 0, qdelta = 0, p = -1, t1 = 0x7fffffff;
   for (;;) {
     int t = 0;
     if (x.lane == 0) asm volatile("atom.shared.add.u32 %0, [%1], 1;" : "=r"(t) : "r"(smem_addr(&S.next)) : "memory");
     t = __shfl_sync(0xffffffffu, t, 0);
-    while (q < kAuxPhases && t >= S.pend[q]) ++q;
-    const int p = q < kAuxPhases ? aux_phase_of(a, q) : -1;
-    int r = q < kAuxPhases ? t + S.pdelta[q] : 0;
+    if (t >= qend) {
+      do {
+        ++q;
+      } while (q < kAuxPhases && t >= S.pend[q]);
+      if (q < kAuxPhases) {
+        p = aux_phase_of(a, q);
+        qend = S.pend[q];
+        qdelta = S.pdelta[q];
+        t1 = p < 6 ? S.pt1[p] : 0x7fffffff;
+      } else {
+        p = -1;
+        qend = 0x7fffffff;
+      }
+    }
+    int r = t + qdelta;
     int bi = 0;   // K3 / level 4-5 / padding tasks: which of the th_cnt images
-    if (p >= 0 && p < 6) {
-      const int t1 = S.pt1[p];
-      while (bi + 1 < kPipeImgs && r >= t1) {
+#pragma unroll
+    for (int i = 1; i < kPipeImgs; ++i)
+      if (r >= t1) {
         r -= t1;
         ++bi;
       }
-    }
     if (a.trace && p >= 0 && x.lane == 0) {   // last task claimed by this warp: start, phase
       trace_rec(a)[40 + (threadIdx.x >> 5)] = gtime();
       trace_rec(a)[56 + (threadIdx.x >> 5)] = p;
