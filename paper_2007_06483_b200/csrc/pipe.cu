@@ -45,6 +45,10 @@ constexpr int kPipeMaxItems = 96;
 #define PIPE_THREADS 512
 #endif
 constexpr int kPipeThreads = PIPE_THREADS;     // 12 K1 warps + 4 aux warps
+#ifndef PIPE_CTAS_PER_SM
+#define PIPE_CTAS_PER_SM 1
+#endif
+constexpr int kPipeCtasPerSm = PIPE_CTAS_PER_SM;   // 2: consecutive launches share an SM (PDL overlap)
 constexpr int kPipeWarps = kPipeThreads / 32;
 constexpr int kK3Units = 4;                     // K3 task = 4 x 32 bitmap words = 4 KB of gray
 constexpr int kK3Words = 32 * kK3Units;
@@ -1059,7 +1063,7 @@ __device__ __forceinline__ void aux_prologue(const PipeArgs& a, PipeSmem& S, int
   named_bar(bar, n);
 }
 
-__global__ void __launch_bounds__(kPipeThreads, 1) pipe_kernel(const __grid_constant__ PipeArgs a,
+__global__ void __launch_bounds__(kPipeThreads, kPipeCtasPerSm) pipe_kernel(const __grid_constant__ PipeArgs a,
                                                              const __grid_constant__ CUtensorMap rgb_map) {
   extern __shared__ __align__(128) uint8_t pipe_smem_raw[];
   const uint32_t raw = smem_addr(pipe_smem_raw);
@@ -1439,7 +1443,7 @@ extern "C" int mtb_align_fused_ex(const uint8_t* rgb, int64_t rgb_pitch, int64_t
     MTB_CUDA(cudaFuncSetAttribute(pipe_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kPipeSmemBytes));
     attr_done = true;
   }
-  const int grid = num_sms();
+  const int grid = num_sms() * kPipeCtasPerSm;
   int launches = 0;
   for (int j = 0; j < J; ++j) {
     a.j = j;
