@@ -112,3 +112,19 @@ def test_fused_matches_staged_24mp(mtb, cuda):
             assert torch.equal(eng.bitmap_words(pyr_f.mtb, i, k), eng.bitmap_words(pyr_s.mtb, i, k)), (i, k)
             assert torch.equal(eng.bitmap_words(pyr_f.excl, i, k), eng.bitmap_words(pyr_s.excl, i, k)), (i, k)
     assert torch.equal(acc_f, acc_s) and torch.equal(errs_f, errs_s)
+
+
+def test_fused_pair_patterns(mtb, cuda):
+    """Two images per launch: pairs across launch boundaries, reversed pairs,
+    self-pairs, repeated images and an odd image count (last launch has one
+    K1 image)."""
+    imgs, _ = _stack(512, 384, 7, seed=77, max_shift=16)
+    pairs = [(1, 2), (2, 1), (6, 0), (3, 5), (0, 6), (4, 4), (5, 3), (0, 1), (6, 5), (2, 6)]
+    _check(mtb, cuda, imgs, pairs, maps=True)
+
+
+def test_fused_many_pairs_one_batch(mtb, cuda):
+    """All 36 ordered-by-index pairs of 9 images in one call (many items per launch)."""
+    imgs, _ = _stack(256, 192, 9, seed=91, max_shift=10)
+    pairs = [(i, j) for i in range(9) for j in range(i + 1, 9)]
+    _check(mtb, cuda, imgs, pairs, maps=False)
