@@ -671,11 +671,13 @@ __device__ __forceinline__ void pipe_search_tile(const PipeArgs& a, const PipeIt
     const int sy0 = y0 - by - 1;
     const int idx0 = j0 - qb - 2 + lane, idx1 = idx0 + 32;
     const bool c0 = idx0 >= 0 && idx0 < nw, c1 = lane < 3 && idx1 >= 0 && idx1 < nw;
-    const int64_t rowoff = (int64_t)sy0 * nw;
-    const uint32_t* pb0 = B + rowoff + (c0 ? idx0 : 0);
-    const uint32_t* peb0 = EB + rowoff + (c0 ? idx0 : 0);
-    const uint32_t* pb1 = B + rowoff + (c1 ? idx1 : 0);
-    const uint32_t* peb1 = EB + rowoff + (c1 ? idx1 : 0);
+    // word idx0 + 32 of the same row (lanes 0-2) is an immediate offset off
+    // the same pointer (a zero-size copy reads nothing, so the clamped base
+    // needs no separate check)
+    const int64_t rowoff = (int64_t)sy0 * nw + (c0 ? idx0 : 0);
+    const uint32_t* pb0 = B + rowoff;
+    const uint32_t* peb0 = EB + rowoff;
+    const int shift1 = c0 ? 32 : idx1;   // pb0 + shift1 = word idx1 when c1
 #pragma unroll
     for (int r = 0; r < kSRows + 2; ++r) {
       const int sy = sy0 + r;
@@ -683,13 +685,11 @@ __device__ __forceinline__ void pipe_search_tile(const PipeArgs& a, const PipeIt
       cp_async4(&sm.b[r][lane], pb0, rok && c0);
       cp_async4(&sm.eb[r][lane], peb0, rok && c0);
       if (lane < 3) {
-        cp_async4(&sm.b[r][lane + 32], pb1, rok && c1);
-        cp_async4(&sm.eb[r][lane + 32], peb1, rok && c1);
+        cp_async4(&sm.b[r][lane + 32], pb0 + shift1, rok && c1);
+        cp_async4(&sm.eb[r][lane + 32], peb0 + shift1, rok && c1);
       }
       pb0 += nw;
       peb0 += nw;
-      pb1 += nw;
-      peb1 += nw;
     }
     asm volatile("cp.async.wait_all;" ::: "memory");
     __syncwarp();
