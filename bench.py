@@ -361,7 +361,7 @@ def run_ours(args, rank, world, local_rank):
                    "correct_offsets": f"{correct}/{P} match ground truth"},
         "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
                      "frac": round(achieved / peak, 4), "traffic": traffic, "peak_source": peak_src,
-                     "kernel": ("pipe_kernel (fused K1+K3+K4, two images per launch, "
+                     "kernel": (f"pipe_kernel (fused K1+K3+K4, {_lib.load().mtb_align_fused_images_per_launch(args.width, args.height)} image(s) per launch, "
                                 f"{n_launch_fused} PDL launches per step)") if fused else
                                f"k1_rgb_pyramid_kernel (K1: RGB->gray->pyramid->histograms, {k1_images} images/launch)",
                      "algorithmic_bytes_per_launch": k1_bytes, "avg_launch_ms": round(k1_avg_s * 1e3, 4),

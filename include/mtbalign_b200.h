@@ -263,10 +263,12 @@ int mtb_align_fused_workspace(int w, int h, int levels, int64_t* gray_bytes, int
  * per-(pair, level) decided flags (zeroed by the call). */
 int64_t mtb_align_fused_sync_words(int n_img, int n_pairs, int levels);
 
-/* Images per launch B of the fused pipeline: launch j runs K1 of images
+/* Images per launch B of the fused pipeline for W x H images (2 when two
+ * images' gray pyramids fit L2 alongside two being read, else 1; env
+ * MTB_PIPE_IMGS overrides): launch j runs K1 of images
  * jB .. jB+B-1 and K3 of the B images before them; pair (r, t) runs its
  * levels in launches max(r, t)/B + 2 ... + levels - 1. */
-int mtb_align_fused_images_per_launch(void);
+int mtb_align_fused_images_per_launch(int w, int h);
 
 /* pipeline.py:80-90 (to_grayscale -> build_pyramid -> build_mtb_pyramid for
  * every image) followed by find_offset (search.py:74-95) for every pair in

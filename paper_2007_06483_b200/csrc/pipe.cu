@@ -89,6 +89,7 @@ struct PipeArgs {
   int probe;                         // diagnostics (MTB_PIPE_PROBE): 1 = no K1 tiles, 2 = no aux tasks
   int j;                             // this launch's index
   int k1_img0, k1_cnt;               // images k1_img0 .. +k1_cnt-1 of the K1 part (k1_cnt may be 0)
+  int gray_slots;                    // gray ring slots in use: 3 x images per launch
   int th_img0, th_cnt;               // images of the K3 part
   int n_items;
   int search_tiles;
@@ -121,7 +122,8 @@ constexpr int kPStages = PIPE_STAGES;
 #define PIPE_IMGS 2
 #endif
 constexpr int kPipeImgs = PIPE_IMGS;          // images per launch (K1 part and K3 part)
-constexpr int kPGraySlots = 3 * kPipeImgs;    // gray ring: written, being read, lagging readers
+constexpr int kPGraySlots = 3 * kPipeImgs;    // gray ring capacity: written, being read, lagging readers
+                                              // (3 x images per launch slots in use)
 constexpr int kAuxPhases = 7;     // aux task phases: K3 levels 0..3, levels 4..5, padding, search
 
 // Per-aux-warp staging of one search warp-tile: 8 output rows x 32 words of
@@ -834,7 +836,7 @@ __device__ __forceinline__ int aux_phase_tasks(const PipeArgs& a, int p) {
   return p < 6 ? a.th_cnt * aux_phase_tasks1(a, p) : a.search_tiles;
 }
 __device__ __forceinline__ const uint8_t* aux_slot(const PipeArgs& a, int b) {
-  return a.g.gray + (int64_t)((a.th_img0 + b) % kPGraySlots) * a.g.gray_img_stride;
+  return a.g.gray + (int64_t)((a.th_img0 + b) % a.gray_slots) * a.g.gray_img_stride;
 }
 __device__ __forceinline__ uint32_t* aux_mtb(const PipeArgs& a, int b) {
   return a.mtb + (int64_t)(a.th_img0 + b) * a.bit_img_words32;
@@ -1150,8 +1152,8 @@ __global__ void __launch_bounds__(kPipeThreads, kPipeCtasPerSm) pipe_kernel(cons
       }
       // gray slot i % kPGraySlots last held image i - kPGraySlots: wait until
       // every CTA has thresholded it
-      if (kt < a.k1_cnt && a.k1_img0 + kt >= kPGraySlots)
-        spin_geq_traced(trace_rec(a), 22, a.k3_done + (a.k1_img0 + kt - kPGraySlots), gridDim.x);
+      if (kt < a.k1_cnt && a.k1_img0 + kt >= a.gray_slots)
+        spin_geq_traced(trace_rec(a), 22, a.k3_done + (a.k1_img0 + kt - a.gray_slots), gridDim.x);
       named_bar(5, 32 * kPK1Warps);   // hist zeroed, mbarriers initialised, slots free
       int k = 0, ptx = 0, pty = 0;
       uint8_t* ptg = nullptr;
@@ -1186,7 +1188,7 @@ __global__ void __launch_bounds__(kPipeThreads, kPipeCtasPerSm) pipe_kernel(cons
         if (k > 0 && a.g.nl >= 5 && wg == ((k - 1) & 3))
           k1_levels45_tm(a.g, ptg, S.l3[g][(k - 1) & 1], ptx, pty, lane, phb, pfull);
         const int img = a.k1_img0 + b;
-        uint8_t* tg = a.g.gray + (int64_t)(img % kPGraySlots) * a.g.gray_img_stride + (int64_t)tile * kTileGrayBytes;
+        uint8_t* tg = a.g.gray + (int64_t)(img % a.gray_slots) * a.g.gray_img_stride + (int64_t)tile * kTileGrayBytes;
         const uint32_t hbi = hb + (uint32_t)b * (6 * 256 * 4);
         uint8_t* l3_slot = &S.l3[g][k & 1][wg][lane];
         if (full)
@@ -1292,7 +1294,18 @@ int64_t spread_hist_elems(int n_levels);
 
 using namespace mtb;
 
-extern "C" int mtb_align_fused_images_per_launch() { return kPipeImgs; }
+// Images per launch: 2 up to 64 MB of gray per image (24 MP = 33 MB: 2
+// images per launch measured 16.7 K vs 16.1 K pairs/s although more gray
+// spills to HBM; 12 MP: 28.2 K vs 24.1 K), else 1.  MTB_PIPE_IMGS overrides.
+static int pipe_images_per_launch(int w, int h) {
+  const char* e = getenv("MTB_PIPE_IMGS");
+  if (e) return std::max(1, std::min(kPipeImgs, atoi(e)));
+  const int64_t slot = (int64_t)((w + kK1TilePx - 1) / kK1TilePx) * ((h + kK1TileRows - 1) / kK1TileRows) *
+                       kTileGrayBytes;
+  return slot <= ((int64_t)64 << 20) ? kPipeImgs : 1;
+}
+
+extern "C" int mtb_align_fused_images_per_launch(int w, int h) { return pipe_images_per_launch(w, h); }
 
 extern "C" int64_t mtb_align_fused_sync_words(int n_img, int n_pairs, int levels) {
   return (int64_t)(n_img + 8) + 2 * (int64_t)n_img + (int64_t)n_pairs * (levels < 1 ? 1 : levels);
@@ -1402,7 +1415,8 @@ extern "C" int mtb_align_fused_ex(const uint8_t* rgb, int64_t rgb_pitch, int64_t
   // Launch j runs K1 of images jB .. jB+B-1 and K3 of images (j-1)B ..
   // (B = kPipeImgs); pair q runs level n-1-(j-t(q)) in launch j, t(q) =
   // max(ref, tgt) / B + 2 (the launch after its images' K3).
-  const int B = kPipeImgs;
+  const int B = pipe_images_per_launch(w, h);
+  a.gray_slots = 3 * B;
   const int k1_launches = (n_img + B - 1) / B;
   std::vector<int> ready(n_pairs);
   int J = k1_launches + 1;

@@ -255,7 +255,7 @@ class MtbEngine:
 
     def fused_launches(self, n_img: int, pairs) -> int:
         """Launch count of align_fused for n_img images and these pairs."""
-        b = int(_lib.load().mtb_align_fused_images_per_launch())
+        b = int(_lib.load().mtb_align_fused_images_per_launch(self.width, self.height))
         j = -(-int(n_img) // b) + 1
         for r, t in pairs:
             j = max(j, max(int(r), int(t)) // b + 2 + self.n)
