@@ -349,8 +349,9 @@ def run_ours(args, rank, world, local_rank):
         "metric": METRIC, "value": round(value, 2), "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": max(3, args.warmup), "ms_per_step": round(elapsed / args.steps * 1e3, 4),
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u8", "data": "synthetic",
-        "config": {"workload": f"{P} x 24MP ({args.width}x{args.height}) RGB8 exposure pairs per GPU per step, "
-                               f"{args.levels} levels, tol {args.tol} (BASELINE config 2, batched)",
+        "config": {"workload": f"{P} x {args.width * args.height / 1e6:.0f}MP ({args.width}x{args.height}) RGB8 exposure pairs per GPU per step, "
+                               f"{args.levels} levels, tol {args.tol} (BASELINE config "
+                               f"{ {(6000, 4000): 2, (1024, 768): 1, (4000, 3000): 4, (40000, 25000): 5}.get((args.width, args.height), 'custom')}, batched)",
                    "width": args.width, "height": args.height, "levels": args.levels, "tol": args.tol,
                    "pairs_per_step_per_gpu": P, "preprocess_chunk_images": chunk, "k1_images_per_launch": k1_images,
                    "discard_gray": not args.keep_gray,
@@ -428,7 +429,7 @@ def main():
                 "steps": args.cpu_reps, "warmup": 1, "ms_per_step": round(1e3 / cb["value"], 2),
                 "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u8",
                 "data": "synthetic", "impl": "reference",
-                "config": {"workload": f"1 x 24MP ({args.width}x{args.height}) RGB8 pair per step, "
+                "config": {"workload": f"1 x {args.width * args.height / 1e6:.0f}MP ({args.width}x{args.height}) RGB8 pair per step, "
                                        f"{args.levels} levels, tol {args.tol}"},
                 "cpu_baseline": cb,
                 "e2e": {"value": round(cb["value"], 4), "unit": UNIT, "h2d_bytes_per_step": 0,
