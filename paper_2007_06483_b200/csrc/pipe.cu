@@ -31,7 +31,9 @@
 // Level-0/1 gray is stored with L2::evict_last (no persisting set-aside: it
 // measured slower); the RGB stream is evict_first.
 #ifndef PIPE_GRAY_EVICT_NORMAL
+#ifndef PIPE_GRAY_EVICT_NORMAL
 #define PIPE_GRAY_EVICT_LAST
+#endif
 #endif
 
 #include "k1_tile.cuh"
