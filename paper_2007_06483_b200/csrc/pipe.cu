@@ -905,7 +905,13 @@ __device__ __forceinline__ void aux_run(const PipeArgs& a, PipeSmem& S, const Au
 // Queue order q -> phase: search tiles first (the longest tasks; their CTA
 // partial counts are flushed as soon as the CTA's last tile is done, so the
 // next launch's level can start early), then K3 levels 0..3, 4..5, padding.
-__device__ __forceinline__ int aux_phase_of(const PipeArgs& a, int q) { return q == 0 ? 6 : q - 1; }
+#ifndef PIPE_SEARCH_Q
+#define PIPE_SEARCH_Q 0
+#endif
+constexpr int kSearchQ = PIPE_SEARCH_Q;   // queue position of the search tiles
+__device__ __forceinline__ int aux_phase_of(const PipeArgs& a, int q) {
+  return q == kSearchQ ? 6 : (q < kSearchQ ? q : q - 1);
+}
 
 __device__ __forceinline__ void aux_stamp(const PipeArgs& a, int i) {
   if (a.trace) {
@@ -1054,7 +1060,7 @@ __device__ __forceinline__ void aux_prologue(const PipeArgs& a, PipeSmem& S, int
   for (int i = at; i < a.n_items * 9; i += n) (&S.scnt[0][0])[i] = 0;
   named_bar(bar, n);
   if (at == 0) {
-    S.sleft = S.pcnt[0];   // queue phase 0 = search tiles
+    S.sleft = S.pcnt[kSearchQ];   // search tiles of this CTA
     int e = 0;
     for (int q = 0; q < kAuxPhases; ++q) {
       S.pdelta[q] = S.plo[q] - e;
@@ -1063,7 +1069,7 @@ __device__ __forceinline__ void aux_prologue(const PipeArgs& a, PipeSmem& S, int
     }
   }
   // a CTA without search tiles still counts towards every item's completion
-  if (S.pcnt[0] == 0 && at < a.n_items) pipe_search_flush(a, a.items[at], S.scnt[at]);
+  if (S.pcnt[kSearchQ] == 0 && at < a.n_items) pipe_search_flush(a, a.items[at], S.scnt[at]);
   named_bar(bar, n);
 }
 
