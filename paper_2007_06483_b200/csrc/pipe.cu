@@ -87,7 +87,6 @@ struct PipeArgs {
   const uint32_t* img_ready;         // [img] nonzero once the image's RGB is in HBM (streamed input), or null
   uint32_t* decided;                 // [P][n] 1 once the (pair, level) offset is published
   int n_launch;
-  int search_first;                  // aux task order (MTB_PIPE_SEARCH_FIRST)
   int probe;                         // diagnostics (MTB_PIPE_PROBE): 1 = no K1 tiles, 2 = no aux tasks
   int j;                             // this launch's index
   int k1_img0, k1_cnt;               // images k1_img0 .. +k1_cnt-1 of the K1 part (k1_cnt may be 0)
@@ -299,43 +298,25 @@ __device__ __forceinline__ void th_word(const uint32_t (&g)[8], const ThConst& c
   ew = e & keep;
 }
 
-// Unit u of the tile-major threshold sequence: 32 bitmap words of one level.
-// Levels 0..3: words in tile order (tile, row, word) — a unit is 1 KB of
-// contiguous gray; levels 4..5: row-major words (a word spans 2 or 4 tiles).
+// Unit u of the threshold sequence: 32 bitmap words of one level.  Levels
+// 0..3 are in tile order (tile, row, word; threshold tasks below); levels
+// 4..5 are row-major words (a word spans 2 or 4 tiles).
 struct ThUnit {
   int k;            // level
   int64_t out;      // bitmap word index within the image's arena (u32), or -1
   int valid;        // valid pixels of the word
-  const uint8_t* p; // levels 0..3: the word's 32 gray bytes
-  int y, j;         // levels 4..5: word coordinates
+  int y, j;         // word coordinates
 };
 
 __device__ __forceinline__ ThUnit th_unit(const PipeArgs& a, const uint8_t* slot, int u, int lane) {
+  // level-4/5 units only (levels 0..3 are threshold tasks of 4 KB)
   ThUnit r;
-  int k = 0;
-#pragma unroll
-  for (int i = 1; i < kPipeMaxLevels; ++i)
-    if (i < a.n && u >= a.th_units0[i]) k = i;
+  const int k = (a.n > 5 && u >= a.th_units0[5]) ? 5 : 4;
   r.k = k;
-  r.p = nullptr;
-  const int f = (u - a.th_units0[k]) * 32 + lane;   // word index in this level's sequence
-  if (k <= 3) {
-    const int wpr = 8 >> k, lwpr = 3 - k;            // words per tile row
-    const int lwpt = 8 - 2 * k;                      // log2 words per tile
-    const int t = f >> lwpt;
-    const int rem = f & ((1 << lwpt) - 1);
-    const int row = rem >> lwpr, c = rem & (wpr - 1);
-    const int ty = t / a.g.tiles_x, tx = t - ty * a.g.tiles_x;
-    r.y = ty * (kK1TileRows >> k) + row;
-    r.j = tx * wpr + c;
-    r.p = slot + (int64_t)t * kTileGrayBytes + tm_off(k) + row * tm_pitch(k) + c * 32;
-    const bool ok = t < a.g.tiles_x * a.g.tiles_y && r.y < a.g.lh[k] && r.j < a.nw32[k];
-    r.out = ok ? a.bit_off32[k] + (int64_t)r.y * a.nw32[k] + r.j : -1;
-  } else {
-    r.y = f / a.nw32[k];
-    r.j = f - r.y * a.nw32[k];
-    r.out = r.y < a.g.lh[k] ? a.bit_off32[k] + f : -1;
-  }
+  const int f = (u - a.th_units0[k]) * 32 + lane;   // row-major word index in the level
+  r.y = f / a.nw32[k];
+  r.j = f - r.y * a.nw32[k];
+  r.out = r.y < a.g.lh[k] ? a.bit_off32[k] + f : -1;
   r.valid = a.g.lw[k] - 32 * r.j;
   return r;
 }
@@ -350,77 +331,6 @@ __device__ __forceinline__ int div_tiles_x(const PipeArgs& a, int t) {
 template <int K>
 __device__ __forceinline__ int th_level_units(const PipeArgs& a) {
   return (int)((((int64_t)a.g.tiles_x * a.g.tiles_y << (8 - 2 * K)) + 31) >> 5);
-}
-
-// One warp iteration: units u0, u0 + nwarps, ... (NU of them).
-// One task of levels 0..3: 4 consecutive units (4 KB of tile-major gray),
-// split in an issue half (addresses + all eight 16-B loads per lane) and a
-// finish half (threshold, store, discard) so a warp can have the next task's
-// loads in flight while it computes the current one.
-constexpr int kK3NU = 4;
-struct K3Task {
-  uint4 v[kK3NU][2];
-  uint32_t goff[kK3NU];  // byte offset of the lane's 32 gray bytes in the slot
-  int out[kK3NU];        // bitmap word (u32) in the image's arena, or -1
-  int valid[kK3NU];      // valid pixels of the word
-  int K;                 // level
-  uint32_t in;           // bit i: unit i exists (load was real)
-};
-
-__device__ __forceinline__ void k3_issue(const PipeArgs& a, const uint8_t* slot, int K, int u0, int lane, K3Task& T) {
-  const int lwpr = 3 - K, wpr = 1 << lwpr;   // words per tile row
-  const int lwpt = 8 - 2 * K;                // log2 words per tile
-  const int rows = kK1TileRows >> K;
-  const int ntiles = a.g.tiles_x * a.g.tiles_y;
-  const int units = (int)((((int64_t)ntiles << lwpt) + 31) >> 5);
-  const int nw = a.nw32[K], lh = a.g.lh[K], lw = a.g.lw[K];
-  const int boff = (int)a.bit_off32[K];
-  const int toff = tm_off(K), tpitch = tm_pitch(K);
-  T.K = K;
-  T.in = 0;
-#pragma unroll
-  for (int i = 0; i < kK3NU; ++i) {
-    const int u = u0 + i;
-    const int f = (u < units ? u : u0) * 32 + lane;
-    const int t = f >> lwpt;
-    const int rem = f & ((1 << lwpt) - 1);
-    const int row = rem >> lwpr, cc = rem & (wpr - 1);
-    const int ty = div_tiles_x(a, t), tx = t - ty * a.g.tiles_x;
-    const int y = ty * rows + row, j = tx * wpr + cc;
-    // lanes past the last tile (levels 2-3 pack several tiles per unit) read
-    // tile 0 and neither store nor discard
-    const bool in = u < units && t < ntiles;
-    T.in |= (uint32_t)in << i;
-    T.goff[i] = (uint32_t)(in ? t : 0) * kTileGrayBytes + toff + row * tpitch + cc * 32;
-    T.out[i] = (in && y < lh && j < nw) ? boff + y * nw + j : -1;
-    T.valid[i] = lw - 32 * j;
-    const uint4* q = reinterpret_cast<const uint4*>(slot + T.goff[i]);
-    T.v[i][0] = __ldcs(q);
-    T.v[i][1] = __ldcs(q + 1);
-  }
-}
-
-__device__ __forceinline__ void k3_finish(const uint8_t* slot, uint32_t* mtb, uint32_t* excl, const ThConst* th,
-                                          uint32_t yt, uint32_t ytl, const K3Task& T, int lane) {
-  const ThConst c = th[T.K];
-#pragma unroll
-  for (int i = 0; i < kK3NU; ++i) {
-    const uint32_t g[8] = {T.v[i][0].x, T.v[i][0].y, T.v[i][0].z, T.v[i][0].w,
-                           T.v[i][1].x, T.v[i][1].y, T.v[i][1].z, T.v[i][1].w};
-    uint32_t m, e;
-    th_word(g, c, yt, ytl, T.valid[i], m, e);
-    if (T.out[i] >= 0) {
-      mtb[T.out[i]] = m;
-      excl[T.out[i]] = e;
-    }
-  }
-  __syncwarp();
-  // 4 consecutive lanes read one 128-B gray line: drop it from L2 without write-back.
-  if ((lane & 3) == 0) {
-#pragma unroll
-    for (int i = 0; i < kK3NU; ++i)
-      if ((T.in >> i) & 1u) asm volatile("discard.global.L2 [%0], 128;" ::"l"(slot + T.goff[i]) : "memory");
-  }
 }
 
 // ---- K3 via TMA bulk copies ------------------------------------------------
@@ -899,9 +809,7 @@ __device__ __forceinline__ void aux_run(const PipeArgs& a, PipeSmem& S, const Au
 // shared-memory counter: the aux warps right after the grid dependency wait,
 // the K1 warps once the image's tiles are exhausted (tiles are claimed
 // dynamically, so every CTA's K1 warps run dry at about the same time and the
-// equal static slices stay balanced).  Task order within the CTA: K3 levels
-// 0..3 (4 units each), levels 4..5, padding, search tiles — or search first
-// (a.search_first).
+// equal static slices stay balanced).
 // Queue order q -> phase: search tiles first (the longest tasks; their CTA
 // partial counts are flushed as soon as the CTA's last tile is done, so the
 // next launch's level can start early), then K3 levels 0..3, 4..5, padding.
@@ -1403,8 +1311,6 @@ extern "C" int mtb_align_fused_ex(const uint8_t* rgb, int64_t rgb_pitch, int64_t
   {
     const char* pr = getenv("MTB_PIPE_PROBE");
     a.probe = pr ? atoi(pr) : 0;
-    const char* sf = getenv("MTB_PIPE_SEARCH_FIRST");
-    a.search_first = sf ? atoi(sf) : 0;
     const char* tr = getenv("MTB_PIPE_TRACE");   // device address of a [J][grid][8] u64 buffer
     a.trace = tr ? reinterpret_cast<unsigned long long*>(strtoull(tr, nullptr, 0)) : nullptr;
   }
