@@ -427,19 +427,26 @@ __device__ __forceinline__ void k3_bulk_units_l0(const PipeArgs& a, uint32_t* mt
   const int y0 = ty * kK1TileRows + ((r & 1) << 4) + (lane >> 3);
   const int valid = a.g.lw[0] - 32 * j;
   const bool ok = j < nw;
+  // running pointers: unit i is 4 rows below unit i-1
   uint32_t* pm = mtb + (int)a.bit_off32[0] + y0 * nw + j;
   uint32_t* pe = excl + (int)a.bit_off32[0] + y0 * nw + j;
+  const uint8_t* src = buf + lane * 32;
+  int rows_left = ok ? lh - y0 : 0;
 #pragma unroll 1
   for (int i = 0; i < kK3Units; ++i) {
-    const uint4 v0 = *reinterpret_cast<const uint4*>(buf + (i * 32 + lane) * 32);
-    const uint4 v1 = *reinterpret_cast<const uint4*>(buf + (i * 32 + lane) * 32 + 16);
+    const uint4 v0 = *reinterpret_cast<const uint4*>(src);
+    const uint4 v1 = *reinterpret_cast<const uint4*>(src + 16);
     const uint32_t g[8] = {v0.x, v0.y, v0.z, v0.w, v1.x, v1.y, v1.z, v1.w};
     uint32_t m, e;
     th_word_t<MED_LO, true>(g, c, yt, ytl, valid, m, e);
-    if (ok && y0 + 4 * i < lh) {
-      pm[4 * i * nw] = m;
-      pe[4 * i * nw] = e;
+    if (rows_left > 0) {
+      *pm = m;
+      *pe = e;
     }
+    src += 32 * 32;
+    pm += 4 * nw;
+    pe += 4 * nw;
+    rows_left -= 4;
   }
 }
 
