@@ -417,6 +417,10 @@ __device__ __forceinline__ void k3_bulk_units(const PipeArgs& a, uint32_t* mtb, 
 
 // Level 0: the task is half a tile (rows 16 (r & 1) .. +15, 8 words each);
 // unit i covers rows +4i .. +4i+3, so tile, column and validity are per task.
+#ifndef K3_L0_UNROLL
+#define K3_L0_UNROLL 1
+#endif
+constexpr int kK3L0Unroll = K3_L0_UNROLL;   // units of a level-0 task interleaved by the compiler
 template <bool MED_LO>
 __device__ __forceinline__ void k3_bulk_units_l0(const PipeArgs& a, uint32_t* mtb, uint32_t* excl, const ThConst& c,
                                                  uint32_t yt, uint32_t ytl, int r, int lane, const uint8_t* buf) {
@@ -432,7 +436,7 @@ __device__ __forceinline__ void k3_bulk_units_l0(const PipeArgs& a, uint32_t* mt
   uint32_t* pe = excl + (int)a.bit_off32[0] + y0 * nw + j;
   const uint8_t* src = buf + lane * 32;
   int rows_left = ok ? lh - y0 : 0;
-#pragma unroll 1
+#pragma unroll kK3L0Unroll
   for (int i = 0; i < kK3Units; ++i) {
     const uint4 v0 = *reinterpret_cast<const uint4*>(src);
     const uint4 v1 = *reinterpret_cast<const uint4*>(src + 16);
