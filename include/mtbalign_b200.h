@@ -270,6 +270,10 @@ int64_t mtb_align_fused_sync_words(int n_img, int n_pairs, int levels);
  * levels in launches max(r, t)/B + 2 ... + levels - 1. */
 int mtb_align_fused_images_per_launch(int w, int h);
 
+/* Number of pipe_kernel launches mtb_align_fused makes for this batch, or -1
+ * on invalid arguments. */
+int mtb_align_fused_launches(int w, int h, int levels, int n_img, const int32_t* pairs_host, int n_pairs);
+
 /* pipeline.py:80-90 (to_grayscale -> build_pyramid -> build_mtb_pyramid for
  * every image) followed by find_offset (search.py:74-95) for every pair in
  * pairs_host [host, n_pairs x (ref, tgt)], as one software-pipelined

@@ -76,6 +76,7 @@ AUX_SIGNATURES = {
     "mtb_align_fused_workspace": ([_i32, _i32, _i32, _i64p, _i64p], ctypes.c_int),
     "mtb_align_fused_sync_words": ([_i32, _i32, _i32], ctypes.c_int64),
     "mtb_align_fused_images_per_launch": ([_i32, _i32], ctypes.c_int),
+    "mtb_align_fused_launches": ([_i32, _i32, _i32, _i32, _c_void_p, _i32], ctypes.c_int),
 }
 
 _lock = threading.Lock()

@@ -148,7 +148,7 @@ struct PipeSmem {
   int next;                                               // aux task queue head
   int plo[kAuxPhases], pcnt[kAuxPhases];                  // this CTA's slice of each aux phase
   int pend[kAuxPhases], pdelta[kAuxPhases];               // queue index end / task = index + delta
-  int sleft;                                              // this CTA's search tiles not yet done
+  int ileft[kPipeMaxItems];                               // this CTA's search tiles of each item not yet done
   int th_state;                                           // 0 idle, 1 being filled, 2 S.th valid
   int k1_warps_done;                                      // K1 warps past their last tile
   int aux_ready;                                          // aux prologue done (queue + slices valid)
@@ -807,12 +807,8 @@ __device__ __forceinline__ void aux_run(const PipeArgs& a, PipeSmem& S, const Au
       if (f < a.th_pad_words) aux_pad(a, aux_mtb(a, b), aux_excl(a, b), f);
       break;
     }
-    default: {
-      int it = 0;
-      while (it + 1 < a.n_items && t >= a.items[it + 1].tile0) ++it;
-      pipe_search_tile(a, a.items[it], t - a.items[it].tile0, x.lane, *x.stage, S.scnt[it]);
-      break;
-    }
+    default:
+      break;   // search tiles: aux_drain
   }
 }
 
@@ -948,18 +944,20 @@ __device__ __forceinline__ void aux_drain(const PipeArgs& a, PipeSmem& S, const 
     if (p == 4) aux_need_thresholds(a, S, x.lane);
     aux_run(a, S, x, p, r, bi);
     if (p == 6) {
-      // last search tile of this CTA: publish its partial counts
+      int it = 0;
+      while (it + 1 < a.n_items && r >= a.items[it + 1].tile0) ++it;
+      pipe_search_tile(a, a.items[it], r - a.items[it].tile0, x.lane, *x.stage, S.scnt[it]);
+      // this CTA's last tile of the item: publish its partial counts (the
+      // item's level can be decided before this CTA's later search tiles)
       __syncwarp();
-      int left = 0;
       if (x.lane == 0) {
         __threadfence_block();
-        left = atomicSub(&S.sleft, 1) - 1;
+        if (atomicSub(&S.ileft[it], 1) == 1) {
+          __threadfence_block();
+          pipe_search_flush(a, a.items[it], S.scnt[it]);
+        }
       }
-      left = __shfl_sync(0xffffffffu, left, 0);
-      if (left == 0) {
-        __threadfence_block();
-        for (int i = x.lane; i < a.n_items; i += 32) pipe_search_flush(a, a.items[i], S.scnt[i]);
-      }
+      __syncwarp();
     }
   }
 }
@@ -979,7 +977,6 @@ __device__ __forceinline__ void aux_prologue(const PipeArgs& a, PipeSmem& S, int
   for (int i = at; i < a.n_items * 9; i += n) (&S.scnt[0][0])[i] = 0;
   named_bar(bar, n);
   if (at == 0) {
-    S.sleft = S.pcnt[kSearchQ];   // search tiles of this CTA
     int e = 0;
     for (int q = 0; q < kAuxPhases; ++q) {
       S.pdelta[q] = S.plo[q] - e;
@@ -987,8 +984,15 @@ __device__ __forceinline__ void aux_prologue(const PipeArgs& a, PipeSmem& S, int
       S.pend[q] = e;
     }
   }
-  // a CTA without search tiles still counts towards every item's completion
-  if (S.pcnt[kSearchQ] == 0 && at < a.n_items) pipe_search_flush(a, a.items[at], S.scnt[at]);
+  // this CTA's tiles of each item; an item it has none of is flushed now
+  // (every CTA counts towards every item's completion)
+  for (int i = at; i < a.n_items; i += n) {
+    const int lo = S.plo[kSearchQ], hi = lo + S.pcnt[kSearchQ];
+    const int t0 = a.items[i].tile0, t1 = i + 1 < a.n_items ? a.items[i + 1].tile0 : a.search_tiles;
+    const int c = max(0, min(hi, t1) - max(lo, t0));
+    S.ileft[i] = c;
+    if (c == 0) pipe_search_flush(a, a.items[i], S.scnt[i]);
+  }
   named_bar(bar, n);
 }
 
@@ -1234,6 +1238,65 @@ static int pipe_images_per_launch(int w, int h) {
 
 extern "C" int mtb_align_fused_images_per_launch(int w, int h) { return pipe_images_per_launch(w, h); }
 
+// Launch plan of one mtb_align_fused call: launch j runs K1 of images
+// jB .. jB+B-1 and K3 of images (j-1)B .. jB-1; pair q runs level
+// n-1-(j-t(q)) in launch j, t(q) = max(ref, tgt) / B + 2 (the launch after
+// its images' K3).  After the last K3 launch only search levels remain:
+// with MTB_PIPE_MERGE=1 they run in ONE launch whose items go coarse to
+// fine (each item's tiles wait for the previous level's decided flag, which
+// every CTA's per-item flush releases) - measured 6 % slower per 32-pair
+// step than one launch per level, so off by default.
+struct PipeLaunch {
+  int j;                                    // launch index (K1/K3 images, tile counter)
+  std::vector<std::pair<int, int>> items;   // (pair, level)
+};
+static std::vector<PipeLaunch> pipe_plan(int n_img, int B, int nl, const int32_t* pairs, int n_pairs) {
+  const int k1_launches = (n_img + B - 1) / B;
+  std::vector<int> ready(n_pairs);
+  int J = k1_launches + 1;
+  for (int q = 0; q < n_pairs; ++q) {
+    const int r = pairs[2 * q], tg = pairs[2 * q + 1];
+    ready[q] = (r > tg ? r : tg) / B + 2;
+    J = std::max(J, ready[q] + nl);
+  }
+  const int jm = k1_launches + 1;   // first launch without K1 / K3 work
+  std::vector<PipeLaunch> plan;
+  for (int j = 0; j < std::min(J, jm); ++j) {
+    PipeLaunch l{j, {}};
+    for (int q = 0; q < n_pairs; ++q) {
+      const int d = j - ready[q];
+      if (d >= 0 && d < nl) l.items.emplace_back(q, nl - 1 - d);
+    }
+    plan.push_back(std::move(l));
+  }
+  if (J > jm) {
+    PipeLaunch m{jm, {}};
+    for (int lev = nl - 1; lev >= 0; --lev)
+      for (int q = 0; q < n_pairs; ++q)
+        if (ready[q] + (nl - 1 - lev) >= jm) m.items.emplace_back(q, lev);
+    const char* mg = getenv("MTB_PIPE_MERGE");
+    if ((int)m.items.size() <= kPipeMaxItems && mg && atoi(mg)) {
+      plan.push_back(std::move(m));
+    } else {
+      for (int j = jm; j < J; ++j) {
+        PipeLaunch l{j, {}};
+        for (int q = 0; q < n_pairs; ++q) {
+          const int d = j - ready[q];
+          if (d >= 0 && d < nl) l.items.emplace_back(q, nl - 1 - d);
+        }
+        plan.push_back(std::move(l));
+      }
+    }
+  }
+  return plan;
+}
+
+extern "C" int mtb_align_fused_launches(int w, int h, int levels, int n_img, const int32_t* pairs_host, int n_pairs) {
+  Plan p;
+  if (!make_plan(w, h, levels, &p) || n_img < 1 || n_pairs < 0 || (n_pairs > 0 && !pairs_host)) return -1;
+  return (int)pipe_plan(n_img, pipe_images_per_launch(w, h), p.n, pairs_host, n_pairs).size();
+}
+
 extern "C" int64_t mtb_align_fused_sync_words(int n_img, int n_pairs, int levels) {
   return (int64_t)(n_img + 8) + 2 * (int64_t)n_img + (int64_t)n_pairs * (levels < 1 ? 1 : levels);
 }
@@ -1337,19 +1400,10 @@ extern "C" int mtb_align_fused_ex(const uint8_t* rgb, int64_t rgb_pitch, int64_t
     MTB_CUDA(cudaMemsetAsync(done, 0, sizeof(uint32_t) * p.n * n_pairs, st));
   }
 
-  // Launch j runs K1 of images jB .. jB+B-1 and K3 of images (j-1)B ..
-  // (B = kPipeImgs); pair q runs level n-1-(j-t(q)) in launch j, t(q) =
-  // max(ref, tgt) / B + 2 (the launch after its images' K3).
   const int B = pipe_images_per_launch(w, h);
   a.gray_slots = 3 * B;
-  const int k1_launches = (n_img + B - 1) / B;
-  std::vector<int> ready(n_pairs);
-  int J = k1_launches + 1;
-  for (int q = 0; q < n_pairs; ++q) {
-    const int r = pairs_host[2 * q], tg = pairs_host[2 * q + 1];
-    ready[q] = (r > tg ? r : tg) / B + 2;
-    if (ready[q] + p.n > J) J = ready[q] + p.n;
-  }
+  const std::vector<PipeLaunch> plan = pipe_plan(n_img, B, p.n, pairs_host, n_pairs);
+  const int J = plan.back().j + 1;
   // sync_ws (mtb_align_fused_sync_words): [J] K1 tile counters, [n_img]
   // medians-ready flags, [n_img] K3-done counters, [P][n] decided flags
   MTB_REQUIRE(J <= n_img + 8, "internal: launch count");
@@ -1359,7 +1413,7 @@ extern "C" int mtb_align_fused_ex(const uint8_t* rgb, int64_t rgb_pitch, int64_t
   a.med_ready = sync_ws + n_img + 8;
   a.k3_done = a.med_ready + n_img;
   a.decided = a.k3_done + n_img;
-  a.n_launch = J;
+  a.n_launch = (int)plan.size();
   int search_tiles_level[kPipeMaxLevels];
   for (int k = 0; k < p.n; ++k) search_tiles_level[k] = ((p.lv[k].h + kSRows - 1) / kSRows) * ((a.nw32[k] + 31) / 32);
 
@@ -1384,7 +1438,8 @@ extern "C" int mtb_align_fused_ex(const uint8_t* rgb, int64_t rgb_pitch, int64_t
   }
   const int grid = num_sms() * kPipeCtasPerSm;
   int launches = 0;
-  for (int j = 0; j < J; ++j) {
+  for (const PipeLaunch& L : plan) {
+    const int j = L.j;
     a.j = j;
     a.k1_img0 = j * B;
     a.k1_cnt = std::max(0, std::min(B, n_img - j * B));
@@ -1392,15 +1447,13 @@ extern "C" int mtb_align_fused_ex(const uint8_t* rgb, int64_t rgb_pitch, int64_t
     a.th_cnt = j >= 1 ? std::max(0, std::min(B, n_img - (j - 1) * B)) : 0;
     a.n_items = 0;
     a.search_tiles = 0;
-    for (int q = 0; q < n_pairs; ++q) {
-      const int d = j - ready[q];
-      if (d < 0 || d >= p.n) continue;
+    for (const auto& qi : L.items) {
       MTB_REQUIRE(a.n_items < kPipeMaxItems, "too many pairs in flight for one fused launch");
       PipeItem& it = a.items[a.n_items++];
-      it.pair = q;
-      it.ref = pairs_host[2 * q];
-      it.tgt = pairs_host[2 * q + 1];
-      it.level = p.n - 1 - d;
+      it.pair = qi.first;
+      it.ref = pairs_host[2 * qi.first];
+      it.tgt = pairs_host[2 * qi.first + 1];
+      it.level = qi.second;
       it.tile0 = a.search_tiles;
       a.search_tiles += search_tiles_level[it.level];
     }

@@ -255,11 +255,9 @@ class MtbEngine:
 
     def fused_launches(self, n_img: int, pairs) -> int:
         """Launch count of align_fused for n_img images and these pairs."""
-        b = int(_lib.load().mtb_align_fused_images_per_launch(self.width, self.height))
-        j = -(-int(n_img) // b) + 1
-        for r, t in pairs:
-            j = max(j, max(int(r), int(t)) // b + 2 + self.n)
-        return j
+        pr = np.ascontiguousarray(np.asarray(pairs, dtype=np.int32).reshape(-1, 2))
+        return int(_lib.load().mtb_align_fused_launches(self.width, self.height, self.requested_levels, int(n_img),
+                                                          pr.ctypes.data, len(pr)))
 
     def align_fused_host(self, host, pairs, pyr: PyramidSet | None = None, acc=None, errs=None, done=None,
                          dev=None, count: bool = True):
