@@ -344,6 +344,9 @@ def run_ours(args, rank, world, local_rank):
     e2e = None
     if not args.no_e2e:
         e2e = run_e2e(args, torch, eng, batch, pyr, table, acc, errs, done, P)
+    with_out = None
+    if fused and not args.no_e2e:
+        with_out = run_with_output(args, torch, eng, batch, pyr, acc, errs, done, P)
 
     out = {
         "metric": METRIC, "value": round(value, 2), "unit": UNIT, "n_gpus": world, "steps": args.steps,
@@ -372,7 +375,41 @@ def run_ours(args, rank, world, local_rank):
     }
     if e2e is not None:
         out["e2e"] = e2e
+    if with_out is not None:
+        out["with_output"] = with_out
     return out
+
+
+def run_with_output(args, torch, eng, batch, pyr, acc, errs, done, P):
+    """SURVEY 8(d) "with output": the step also writes every target aligned
+    onto its reference (shift_rgb of image 2p+1 by pair p's offset, fill 0;
+    image.py:82-93), read from and written to HBM: +6 W H bytes per pair."""
+    from paper_2007_06483_b200 import _lib
+
+    w, h = args.width, args.height
+    out = torch.empty((P, h, w, 3), dtype=torch.uint8, device="cuda")
+    pairs = [(2 * p, 2 * p + 1) for p in range(P)]
+    stream = torch.cuda.current_stream()
+
+    def step():
+        eng.align_fused(batch, pairs, pyr, acc, errs, done, count=False)
+        offs = acc[:, 0].contiguous()   # (P, 2) int32 on the device: no host round trip
+        _lib.call("mtb_shift_rgb", batch[1].data_ptr(), 3 * w, 2 * 3 * w * h, w, h, P, offs.data_ptr(),
+                  0, 0, 0, out.data_ptr(), 3 * w, 3 * w * h, stream.cuda_stream)
+
+    for _ in range(3):
+        step()
+    torch.cuda.synchronize()
+    steps = 20
+    s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    s.record(stream)
+    for _ in range(steps):
+        step()
+    e.record(stream)
+    torch.cuda.synchronize()
+    dt = s.elapsed_time(e) / 1e3
+    return {"value": round(P * steps / dt, 2), "unit": UNIT,
+            "bytes_per_pair": 12 * w * h, "note": "align_fused + shift_rgb of each target (device offsets), python launches"}
 
 
 def run_e2e(args, torch, eng, batch, pyr, table, acc, errs, done, P):
