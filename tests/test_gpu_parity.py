@@ -357,6 +357,27 @@ def test_shift_rgb_gray_vs_oracle(mtb):
     assert (mtb.shift_gray(big, mtb.ShiftOffset(100, 0), fill=7) == 7).all()
 
 
+def test_shift_rgb_vector_path_vs_oracle(mtb, cuda):
+    """Rows of 3W % 16 == 0 take the 16-px vector kernel (PRMT byte funnels over
+    aligned 16-B loads): every source misalignment, borders, fill, batches."""
+    torch = cuda
+    from paper_2007_06483_b200.image import shift_rgb_device
+    rs = np.random.RandomState(11)
+    for w, h in [(16, 5), (64, 9), (160, 33), (208, 17)]:
+        imgs = rs.randint(0, 256, size=(6, h, w, 3), dtype=np.uint8)
+        offs = [(int(d), int(rs.randint(-h, h + 1))) for d in rs.randint(-w - 3, w + 4, size=6)]
+        offs[0] = (0, 0)
+        offs[1] = (1, -1)
+        fill = (5, 250, 17)
+        out = shift_rgb_device(torch.from_numpy(imgs).cuda(), offs, fill).cpu().numpy()
+        for i, (dx, dy) in enumerate(offs):
+            assert np.array_equal(out[i], orc.shift_raster(imgs[i], dx, dy, fill)), (w, h, dx, dy)
+    img = rs.randint(0, 256, size=(7, 48, 3), dtype=np.uint8)
+    for dx in range(-20, 21):   # all 16 source byte alignments, both directions
+        assert np.array_equal(mtb.shift_rgb(img, mtb.ShiftOffset(dx, 2), (1, 2, 3)),
+                              orc.shift_raster(img, dx, 2, (1, 2, 3))), dx
+
+
 def test_generate_stack_matches_reference_recipe(mtb):
     rng = np.random.default_rng(4)
     base = np.dstack([orc.smooth_gray(rng, 96, 80) for _ in range(3)])
