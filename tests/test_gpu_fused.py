@@ -128,3 +128,13 @@ def test_fused_many_pairs_one_batch(mtb, cuda):
     imgs, _ = _stack(256, 192, 9, seed=91, max_shift=10)
     pairs = [(i, j) for i in range(9) for j in range(i + 1, 9)]
     _check(mtb, cuda, imgs, pairs, maps=False)
+
+
+@pytest.mark.parametrize("w,h,n_img", [(16, 16, 1), (48, 20, 3), (512, 384, 1)])
+def test_fused_preprocess_only_and_tiny(mtb, cuda, w, h, n_img):
+    """No pairs (preprocess only), a single image, and the 16x16 minimum (one level)."""
+    rs = np.random.RandomState(w * h + n_img)
+    imgs = [rs.randint(0, 256, size=(h, w, 3), dtype=np.uint8) for _ in range(n_img)]
+    _check(mtb, cuda, imgs, [], levels=6)
+    if n_img >= 2:
+        _check(mtb, cuda, imgs, [(0, n_img - 1)], levels=6)
