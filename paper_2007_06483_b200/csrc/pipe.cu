@@ -824,8 +824,17 @@ __device__ __forceinline__ void aux_run(const PipeArgs& a, PipeSmem& S, const Au
 #define PIPE_SEARCH_Q 0
 #endif
 constexpr int kSearchQ = PIPE_SEARCH_Q;   // queue position of the search tiles
+#ifndef PIPE_K3_ORDER
+#define PIPE_K3_ORDER 0
+#endif
 __device__ __forceinline__ int aux_phase_of(const PipeArgs& a, int q) {
-  return q == kSearchQ ? 6 : (q < kSearchQ ? q : q - 1);
+  const int k = q == kSearchQ ? 6 : (q < kSearchQ ? q : q - 1);
+  if (PIPE_K3_ORDER == 1 && k < 4) {
+    // the latency-bound gathered levels 3 and 2 first, level 0 and 1 last
+    constexpr int order[4] = {3, 2, 0, 1};
+    return k == 0 ? order[0] : (k == 1 ? order[1] : (k == 2 ? order[2] : order[3]));
+  }
+  return k;
 }
 
 __device__ __forceinline__ void aux_stamp(const PipeArgs& a, int i) {
