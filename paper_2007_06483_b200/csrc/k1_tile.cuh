@@ -291,7 +291,9 @@ __device__ __forceinline__ void k1_block_tm(const K1Args& a, uint8_t* tg, const 
         if (FULL || (row_ok && 3 < nv1)) hinc(hb1 | (s3 & 0x3fcu));
         const uint32_t x01 = (s0 + (s1 << 16)) >> 2, x23 = (s2 + (s3 << 16)) >> 2;
         l1[rp] = __byte_perm(x01, x23, 0x6420);
+#ifndef PIPE_PROBE_NO_L123
         st4p(p1 + rp * tm_pitch(1), l1[rp] TM_POLARG);
+#endif
       }
     }
   }
@@ -309,7 +311,9 @@ __device__ __forceinline__ void k1_block_tm(const K1Args& a, uint8_t* tg, const 
       if (FULL || (row_ok && 0 < nv2)) hinc(hb2 | (s0 & 0x3fcu));
       if (FULL || (row_ok && 1 < nv2)) hinc(hb2 | (s1 & 0x3fcu));
       l2[r] = ((s0 >> 2) & 0xffu) | ((s1 << 6) & 0xff00u);
+#ifndef PIPE_PROBE_NO_L123
       *reinterpret_cast<unsigned short*>(p2 + r * tm_pitch(2)) = (unsigned short)l2[r];
+#endif
     }
   }
   if (a.nl < 4) return;

@@ -746,9 +746,13 @@ __device__ __forceinline__ int aux_phase_tasks1(const PipeArgs& a, int p) {
   const bool th = a.th_cnt > 0;
   switch (p) {
     case 0: return th ? (th_level_units<0>(a) + kK3Units - 1) / kK3Units : 0;
+#ifdef PIPE_PROBE_NO_L123   // diagnostics only (wrong maps): no level 1-3 gray stores / thresholds
+    case 1: case 2: case 3: return 0;
+#else
     case 1: return th && a.n > 1 ? (th_level_units<1>(a) + kK3Units - 1) / kK3Units : 0;
     case 2: return th && a.n > 2 ? (th_level_units<2>(a) + kK3Units - 1) / kK3Units : 0;
     case 3: return th && a.n > 3 ? (th_level_units<3>(a) + kK3Units - 1) / kK3Units : 0;
+#endif
     case 4: return th ? a.th_units0[a.n] - a.th_units0[a.n < 4 ? a.n : 4] : 0;
     case 5: return th ? (a.th_pad_words + 31) / 32 : 0;
     default: return a.search_tiles;   // 6
