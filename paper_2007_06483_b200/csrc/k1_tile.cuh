@@ -291,8 +291,8 @@ __device__ __forceinline__ void k1_block_tm(const K1Args& a, uint8_t* tg, const 
         if (FULL || (row_ok && 3 < nv1)) hinc(hb1 | (s3 & 0x3fcu));
         const uint32_t x01 = (s0 + (s1 << 16)) >> 2, x23 = (s2 + (s3 << 16)) >> 2;
         l1[rp] = __byte_perm(x01, x23, 0x6420);
-#ifndef PIPE_PROBE_NO_L123
-        st4p(p1 + rp * tm_pitch(1), l1[rp] TM_POLARG);
+#if defined(PIPE_L1_TASKS) && !defined(PIPE_PROBE_NO_L123)
+        st4p(p1 + rp * tm_pitch(1), l1[rp] TM_POLARG);   // else the level-0 threshold tasks derive level 1
 #endif
       }
     }

@@ -454,6 +454,41 @@ __device__ __forceinline__ void k3_bulk_units_l0(const PipeArgs& a, uint32_t* mt
   }
 }
 
+#ifndef PIPE_L1_TASKS
+// Level 1 of a level-0 task's half tile, derived from its staged level-0
+// rows (pyramid.py:17-32, the same rounding as K1's level 1, so the bits
+// match the median K1's level-1 histogram gave): 16 x 256 px -> 8 x 128 px =
+// 32 words, one per lane (row lane/4, word lane%4), thresholded and stored.
+// K1 therefore never writes level-1 gray and there are no level-1 tasks.
+__device__ __forceinline__ void k3_level1_from_l0(const PipeArgs& a, uint32_t* mtb, uint32_t* excl, const ThConst& c1,
+                                                  uint32_t yt, uint32_t ytl, int r, int lane, const uint8_t* buf) {
+  const int r1 = lane >> 2, c = lane & 3;
+  const uint8_t* up = buf + (2 * r1) * kK1TilePx + 64 * c;
+  uint32_t g[8];
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {   // 16 L0 px of each row -> 8 L1 px = g[2q], g[2q+1]
+    const uint4 u = *reinterpret_cast<const uint4*>(up + 16 * q);
+    const uint4 d = *reinterpret_cast<const uint4*>(up + kK1TilePx + 16 * q);
+    const uint32_t uw[4] = {u.x, u.y, u.z, u.w}, dw[4] = {d.x, d.y, d.z, d.w};
+    uint32_t x[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) x[k] = (box_sum(uw[k], dw[k], 0) + (box_sum(uw[k], dw[k], 1) << 16)) >> 2;
+    g[2 * q] = __byte_perm(x[0], x[1], 0x6420);
+    g[2 * q + 1] = __byte_perm(x[2], x[3], 0x6420);
+  }
+  const int t = r >> 1;
+  const int ty = div_tiles_x(a, t), tx = t - ty * a.g.tiles_x;
+  const int y = ty * (kK1TileRows / 2) + 8 * (r & 1) + r1, j = tx * 4 + c;
+  uint32_t m, e;
+  th_word(g, c1, yt, ytl, a.g.lw[1] - 32 * j, m, e);   // generic form: smaller code measured faster here
+  if (y < a.g.lh[1] && j < a.nw32[1]) {
+    const int o = (int)a.bit_off32[1] + y * a.nw32[1] + j;
+    mtb[o] = m;
+    excl[o] = e;
+  }
+}
+#endif
+
 __device__ __forceinline__ void k3_bulk_finish(const PipeArgs& a, const uint8_t* slot, uint32_t* mtb, uint32_t* excl,
                                                const ThConst* th, uint32_t yt, uint32_t ytl, int K, int r, int lane,
                                                const uint8_t* buf, unsigned long long* bar, uint32_t parity) {
@@ -490,6 +525,9 @@ __device__ __forceinline__ void k3_bulk_finish(const PipeArgs& a, const uint8_t*
   } else {
     k3_bulk_units<false>(a, mtb, excl, c, yt, ytl, K, r, lane, buf);
   }
+#ifndef PIPE_L1_TASKS
+  if (K == 0 && a.n > 1) k3_level1_from_l0(a, mtb, excl, th[1], yt, ytl, r, lane, buf);
+#endif
   const int lwpt = 8 - 2 * K, wpt = 1 << lwpt;
   const int ntiles = a.g.tiles_x * a.g.tiles_y;
   // line `lane` of the task's gray: drop it from L2 without write-back
@@ -748,6 +786,10 @@ __device__ __forceinline__ int aux_phase_tasks1(const PipeArgs& a, int p) {
     case 0: return th ? (th_level_units<0>(a) + kK3Units - 1) / kK3Units : 0;
 #ifdef PIPE_PROBE_NO_L123   // diagnostics only (wrong maps): no level 1-3 gray stores / thresholds
     case 1: case 2: case 3: return 0;
+#elif !defined(PIPE_L1_TASKS)
+    case 1: return 0;   // level 1 is derived inside the level-0 tasks
+    case 2: return th && a.n > 2 ? (th_level_units<2>(a) + kK3Units - 1) / kK3Units : 0;
+    case 3: return th && a.n > 3 ? (th_level_units<3>(a) + kK3Units - 1) / kK3Units : 0;
 #else
     case 1: return th && a.n > 1 ? (th_level_units<1>(a) + kK3Units - 1) / kK3Units : 0;
     case 2: return th && a.n > 2 ? (th_level_units<2>(a) + kK3Units - 1) / kK3Units : 0;

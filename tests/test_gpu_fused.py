@@ -138,3 +138,10 @@ def test_fused_preprocess_only_and_tiny(mtb, cuda, w, h, n_img):
     _check(mtb, cuda, imgs, [], levels=6)
     if n_img >= 2:
         _check(mtb, cuda, imgs, [(0, n_img - 1)], levels=6)
+
+
+@pytest.mark.parametrize("tol", [0, 127, 128, 200])
+def test_fused_tolerances(mtb, cuda, tol):
+    """Exclusion tolerance edge values (tol > 127 takes the generic compare)."""
+    imgs, _ = _stack(512, 384, 2, seed=tol + 3, max_shift=9)
+    _check(mtb, cuda, imgs, [(0, 1)], tol=tol)
