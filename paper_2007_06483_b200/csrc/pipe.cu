@@ -871,12 +871,14 @@ __device__ __forceinline__ void aux_run(const PipeArgs& a, PipeSmem& S, const Au
 #endif
 constexpr int kSearchQ = PIPE_SEARCH_Q;   // queue position of the search tiles
 #ifndef PIPE_K3_ORDER
-#define PIPE_K3_ORDER 0
+#define PIPE_K3_ORDER 1
 #endif
 __device__ __forceinline__ int aux_phase_of(const PipeArgs& a, int q) {
   const int k = q == kSearchQ ? 6 : (q < kSearchQ ? q : q - 1);
   if (PIPE_K3_ORDER == 1 && k < 4) {
-    // the latency-bound gathered levels 3 and 2 first, level 0 and 1 last
+    // the latency-bound gathered levels 3 and 2 first, level 0 (with level 1
+    // derived in it) last, so the CTA's final tasks are the cheap contiguous
+    // ones (+0.8 % at 24 MP, +0.2 % at 12 MP)
     constexpr int order[4] = {3, 2, 0, 1};
     return k == 0 ? order[0] : (k == 1 ? order[1] : (k == 2 ? order[2] : order[3]));
   }
