@@ -1,27 +1,33 @@
 // The fused alignment pipeline: preprocess (K1 + medians + K3) and the
 // coarse-to-fine search (K4) of a whole batch of exposure pairs, software-
-// pipelined over ONE launch per image so the gray pyramids never leave L2.
+// pipelined over persistent launches of B images each (B = 2 up to 64 MB of
+// gray per image) so the gray pyramids stay in L2 as far as they fit.
 //
 // Reference path (bit-exact): pipeline.py:80-90 -> build_mtb_pyramid
 // (image.py:58-68, pyramid.py:17-62, threshold.py:25-88) -> find_offset
 // (search.py:53-95, kernels/_native.pyx:73-111).
 //
-// Launch j (one 512-thread CTA per SM, programmatic dependent launches):
-//   1. TMA-prefetch this CTA's first RGB tiles of image j      (independent)
-//   2. griddepcontrol.wait: launch j-1 (and so every earlier one) is complete
-//   3. medians of image j-1 from its histograms (every CTA, redundantly)
-//   4. K3: threshold + bit-pack every level of image j-1, reading its gray
-//      from L2 (written by launch j-1 with evict_last) and discarding the
-//      consumed lines so they are never written back
-//   5. K4: one pyramid level for every pair whose maps are ready — pair q
-//      (ref, tgt) is ready at t(q) = max(ref, tgt) + 2 and runs level
-//      n-1-(j-t(q)) in launch j; the warp that completes a (pair, level)
-//      applies the search.py:67 key and publishes the offset for launch j+1
-//   6. K1: gray + pyramid (levels 0..5) + histograms of image j into the gray
-//      slot j % 2 (slot (j-2) % 2 was consumed by launch j-1, which is
-//      complete after step 2)
-// HBM traffic per image is the RGB read plus the packed maps; the gray
-// round trip (32 MB per 24 MP image) stays in L2.
+// Launch j (one 512-thread CTA per SM; programmatic dependent launch, and
+// every cross-launch dependency is an acquire/release flag, never a grid
+// wait):
+//   * warps 0-11 (3 groups of 4): K1 of images jB .. jB+B-1 — TMA tile
+//     copies into a 2-stage ring per group, gray + levels 1-5 + per-image
+//     histograms, gray stored tile-major into ring slot i % 3B (levels 0, 2-5;
+//     level 1 is re-derived by K3); the CTA flushes its histograms and the
+//     last CTA of an image publishes its medians (med_ready flag); then they
+//     join the aux queue.
+//   * warps 12-15 from the start, 0-11 once their tiles run out: this CTA's
+//     static slice of the aux queue — search tiles of every (pair, level) due
+//     in this launch (each waits for the previous level's decided flag; a
+//     CTA's partial counts of an item are flushed when its last tile of the
+//     item is done, the last CTA applies the search.py:67 key), then K3 of
+//     the B images of launch j-1: levels 3 and 2 (gathered pieces), level 0
+//     half tiles (one 4 KB TMA bulk copy each, level 1 derived from the staged
+//     rows), levels 4-5, row padding; consumed gray lines are discarded.
+//   * the CTA's end adds itself to each K3 image's done count (gates the
+//     gray slot's reuse three launches on and the pair's first search level).
+// HBM traffic per image is the RGB read, the packed maps and whatever gray
+// the L2 cannot hold (measured in DESIGN.md 4.3).
 #include <algorithm>
 #include <cstdlib>
 #include <cstring>
