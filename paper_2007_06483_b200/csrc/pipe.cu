@@ -865,13 +865,14 @@ __device__ __forceinline__ void aux_run(const PipeArgs& a, PipeSmem& S, const Au
 }
 
 // The CTA's share of every phase's tasks, pulled by its warps from a
-// shared-memory counter: the aux warps right after the grid dependency wait,
-// the K1 warps once the image's tiles are exhausted (tiles are claimed
-// dynamically, so every CTA's K1 warps run dry at about the same time and the
-// equal static slices stay balanced).
-// Queue order q -> phase: search tiles first (the longest tasks; their CTA
-// partial counts are flushed as soon as the CTA's last tile is done, so the
-// next launch's level can start early), then K3 levels 0..3, 4..5, padding.
+// shared-memory counter: the aux warps right after their prologue, the K1
+// warps once the images' tiles are exhausted (tiles are claimed dynamically,
+// so every CTA's K1 warps run dry at about the same time and the equal static
+// slices stay balanced).
+// Queue order q -> phase: search tiles first (their CTA partial counts are
+// flushed per item as soon as the CTA's last tile of it is done, so the next
+// launch's level can start early), then K3 levels 3, 2, 0 (+1), [1: no tasks],
+// 4..5, padding (PIPE_K3_ORDER; PIPE_SEARCH_Q moves the search tiles).
 #ifndef PIPE_SEARCH_Q
 #define PIPE_SEARCH_Q 0
 #endif
