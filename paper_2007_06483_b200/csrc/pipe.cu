@@ -178,7 +178,10 @@ __device__ __forceinline__ uint32_t ld_acquire(const uint32_t* p) {
   return v;
 }
 __device__ __forceinline__ void spin_geq(const uint32_t* p, uint32_t v) {
-  while (ld_acquire(p) < v) __nanosleep(100);
+#ifndef PIPE_SPIN_NS
+#define PIPE_SPIN_NS 100
+#endif
+  while (ld_acquire(p) < v) __nanosleep(PIPE_SPIN_NS);
 }
 
 // Diagnostics (MTB_PIPE_TRACE): kTraceWords u64 per (launch, CTA).
