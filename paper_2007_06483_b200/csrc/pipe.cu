@@ -1364,8 +1364,16 @@ extern "C" int mtb_align_fused_launches(int w, int h, int levels, int n_img, con
   return (int)pipe_plan(n_img, pipe_images_per_launch(w, h), p.n, pairs_host, n_pairs).size();
 }
 
+extern "C" int64_t mtb_resident_sync_words(int n_img, int n_pairs, int levels);
+extern "C" int mtb_resident_supported(int w, int h, int levels, int64_t rgb_pitch, int64_t rgb_img_stride);
+int mtb_resident_run(const uint8_t* rgb, int64_t rgb_pitch, int64_t rgb_img_stride, int w, int h, int n_img,
+                     int levels, int tol, const int32_t* pairs_host, int n_pairs, uint32_t* hist_ws,
+                     int32_t* medians, uint64_t* mtb, uint64_t* exclusion, int32_t* acc, unsigned long long* errs,
+                     uint32_t* done, uint32_t* sync_ws, const uint32_t* img_ready, void* stream);
+
 extern "C" int64_t mtb_align_fused_sync_words(int n_img, int n_pairs, int levels) {
-  return (int64_t)(n_img + 8) + 2 * (int64_t)n_img + (int64_t)n_pairs * (levels < 1 ? 1 : levels);
+  const int64_t pipe = (int64_t)(n_img + 8) + 2 * (int64_t)n_img + (int64_t)n_pairs * (levels < 1 ? 1 : levels);
+  return std::max(pipe, mtb_resident_sync_words(n_img, n_pairs, levels));
 }
 
 extern "C" int mtb_align_fused_workspace(int w, int h, int levels, int64_t* gray_bytes, int64_t* hist_elems) {
@@ -1401,6 +1409,14 @@ extern "C" int mtb_align_fused_ex(const uint8_t* rgb, int64_t rgb_pitch, int64_t
     MTB_REQUIRE(pairs_host[2 * q] >= 0 && pairs_host[2 * q] < n_img && pairs_host[2 * q + 1] >= 0 &&
                     pairs_host[2 * q + 1] < n_img,
                 "pair image index out of range");
+  }
+  {
+    const char* impl = getenv("MTB_FUSED_IMPL");
+    const bool force_pipe = impl && std::strcmp(impl, "pipe") == 0;
+    if (!force_pipe && mtb_resident_supported(w, h, levels, rgb_pitch, rgb_img_stride) &&
+        (reinterpret_cast<uintptr_t>(rgb) & 7) == 0)
+      return mtb_resident_run(rgb, rgb_pitch, rgb_img_stride, w, h, n_img, levels, tol, pairs_host, n_pairs,
+                              hist_ws, medians, mtb, exclusion, acc, errs, done, sync_ws, img_ready, stream);
   }
   cudaStream_t st = as_stream(stream);
 
