@@ -35,6 +35,8 @@
 // HBM traffic per image: the RGB read once (72 MB at 24 MP) plus the packed
 // maps (8 MB written, read back by the search from L2).
 #include <algorithm>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <vector>
 
@@ -51,20 +53,20 @@ constexpr int kRWarps = kRThreads / 32;
 constexpr int kRSearchWarps = RES_SEARCH_WARPS;
 constexpr int kRK1Warps = kRWarps - kRSearchWarps;
 constexpr int kJobRows = 32, kJobPx = 64;
-constexpr int kSlotBytes = 2736;          // L0 2048 + L1 512 + L2 128 + L3 32 + L4 8 + L5 2 (16-B multiple)
+constexpr int kSlotBytes = 2224;          // L0 2048 + L2 128 + L3 32 + L4 8 + L5 2 (level 1 is derived in K3)
+constexpr int kStageBytes = kJobRows * 3 * kJobPx;   // one job's RGB: 32 rows x 192 B (TMA box 48 u32 x 32 rows)
+constexpr int kRMaxStages = 8;
 constexpr int kRMaxLevels = 6;
 constexpr int kRSearchRows = 32;          // search task: 32 output rows x 32 words
 constexpr int kRSmemLimit = 232448;       // opt-in dynamic + static shared memory per CTA on sm_100
 constexpr int kRMaxPairsPerUpload = 1536;
 
 __host__ __device__ constexpr int slot_off(int k) {
-  return k == 0 ? 0 : k == 1 ? 2048 : k == 2 ? 2560 : k == 3 ? 2688 : k == 4 ? 2720 : 2728;
+  return k == 0 ? 0 : k == 2 ? 2048 : k == 3 ? 2176 : k == 4 ? 2208 : 2216;
 }
 // Level 0: row i (0..31) of 64 px, 16-B chunk q (0..3), XOR-swizzled so the
 // K3 reads (lane = row, 16 B per lane) and the K1 stores are bank-conflict free.
 __device__ __forceinline__ int l0_addr(int row, int q) { return row * 64 + 16 * (q ^ (((row >> 1) ^ (row >> 3)) & 3)); }
-// Level 1: row i (0..15) of 32 px, chunk q (0..1).
-__device__ __forceinline__ int l1_addr(int row, int q) { return slot_off(1) + row * 32 + 16 * (q ^ ((row >> 2) & 1)); }
 
 struct ResArgs {
   const uint8_t* rgb;
@@ -77,8 +79,9 @@ struct ResArgs {
   int n_img;
   uint32_t* mtb;
   uint32_t* excl;
-  uint32_t* hist;                   // spread histograms [img][level][bin * 32]
-  int64_t hist_img_stride;
+  uint32_t* part;                   // [2][G][6 * 256] partial histograms of each CTA (image parity)
+  uint32_t* tot;                    // [2][6 * 256] summed histograms
+  uint32_t* arrive2;                // [n_img] CTAs that summed their bins of the image
   int32_t* medians;                 // [img][n]
   int n_pairs;
   const int32_t* pairs;             // device [P][2] (ref, tgt)
@@ -92,9 +95,25 @@ struct ResArgs {
   uint32_t* qitem;                  // [P * n] search queue: 0 = empty, else pair * 8 + level + 1
   uint32_t* qclaim;                 // [P * n] claimed tasks of each queue entry
   uint32_t* qtail;                  // entries appended
+  uint32_t* medflag;                // [G][32] per-CTA line: [0] images flushed, [1] images with medians, [2..7] medians
   const uint32_t* img_ready;        // [n_img] nonzero once the image's RGB is in HBM (streamed input), or null
   int tasks[kRMaxLevels], strips[kRMaxLevels];
+  int stages;                       // TMA ring depth
+#ifdef RES_EXP_TRACE   // experiment builds only: [n_img][G][4] %globaltimer stamps
+  unsigned long long* trace;
+#endif
 };
+
+#ifdef RES_EXP_TRACE
+__device__ __forceinline__ void rtrace(const ResArgs& a, int s, int what) {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  a.trace[((int64_t)s * gridDim.x + blockIdx.x) * 8 + what] = t;
+}
+#define RTRACE(a, s, w) rtrace(a, s, w)
+#else
+#define RTRACE(a, s, w)
+#endif
 
 // Threshold constants of one level (threshold.py:42-56).
 struct RTh {
@@ -103,15 +122,39 @@ struct RTh {
 };
 
 struct ResShared {
+  unsigned long long full[kRMaxStages];   // TMA ring: job RGB landed
+  int stage_job[kRMaxStages];             // job whose copy was issued into each stage
   RTh th[2][kRMaxLevels];  // threshold constants of images s (parity s & 1)
   int medtag[2];           // s + 1 once th[s & 1] holds image s's constants
   int medclaim[2];         // s + 1 once a warp computes them
   int k1cnt[2], k3cnt[2];  // K1 / K3 jobs finished of image s (parity s & 1)
   int claim;               // job sequence counter
   int ready_img;           // streamed input: images known to be in HBM
+  int stages;              // TMA ring depth
 };
 
 // ---- memory-model helpers ---------------------------------------------------
+// Spins poll with relaxed loads (L2, no L1 invalidation) and acquire once the
+// condition holds: an acquire load at gpu scope invalidates the SM's L1
+// (CCTL.IVALL), which would throw away the K1 warps' RGB lines on every poll.
+__device__ __forceinline__ uint32_t r_ld_relaxed(const uint32_t* p) {
+  uint32_t v;
+  asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void r_fence_acquire() { asm volatile("fence.acq_rel.gpu;" ::: "memory"); }
+__device__ __forceinline__ void r_spin_geq(const uint32_t* p, uint32_t v, int ns) {
+  while (r_ld_relaxed(p) < v) __nanosleep(ns);
+  r_fence_acquire();
+}
+__device__ __forceinline__ int r_ld_acquire_cta(const int* p) {
+  int v;
+  asm volatile("ld.acquire.cta.shared::cta.u32 %0, [%1];" : "=r"(v) : "r"(smem_addr(p)) : "memory");
+  return v;
+}
+__device__ __forceinline__ void r_st_release_cta(int* p, int v) {
+  asm volatile("st.release.cta.shared::cta.u32 [%0], %1;" ::"r"(smem_addr(p)), "r"(v) : "memory");
+}
 __device__ __forceinline__ uint32_t r_ld_acquire(const uint32_t* p) {
   uint32_t v;
   asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
@@ -121,6 +164,9 @@ __device__ __forceinline__ uint32_t r_atom_add_acqrel(uint32_t* p, uint32_t v) {
   uint32_t old;
   asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], %2;" : "=r"(old) : "l"(p), "r"(v) : "memory");
   return old;
+}
+__device__ __forceinline__ void r_st_relaxed(uint32_t* p, uint32_t v) {
+  asm volatile("st.relaxed.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
 __device__ __forceinline__ void r_st_release(uint32_t* p, uint32_t v) {
   asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
@@ -133,53 +179,26 @@ __device__ __forceinline__ int r_smem_add_acqrel(int* p, int v) {
                : "memory");
   return old;
 }
-__device__ __forceinline__ uint2 ldg64_first(const uint8_t* p, uint64_t pol) {
-  uint2 v;
-  asm volatile("ld.global.L2::cache_hint.v2.u32 {%0, %1}, [%2], %3;" : "=r"(v.x), "=r"(v.y) : "l"(p), "l"(pol));
-  return v;
-}
-
 // ---- K1: gray, levels 1..5, histograms of one job (one warp) --------------
-// Lane (r = lane >> 3, c = lane & 7) owns the 8x8 px block at job row 8r,
-// column 8c: v[i][0..2] = the 24 RGB bytes of its row i.
-template <bool FULL>
-__device__ __forceinline__ void res_load(const ResArgs& a, int img, int jx, int jy, int lane, uint2 (&v)[8][3],
-                                         uint64_t pol) {
-  const int r = lane >> 3, c = lane & 7;
-  const int x0 = jx * kJobPx + 8 * c, y0 = jy * kJobRows + 8 * r;
-  const uint8_t* p = a.rgb + (int64_t)img * a.rgb_img_stride + (int64_t)y0 * a.rgb_pitch + 3 * x0;
-  if (FULL) {
+// The job's RGB (32 rows x 192 B) lands in a shared-memory stage by one TMA
+// tile copy; lane (r = lane >> 3, c = lane & 7) copies its 8x8 px block
+// (v[i][0..2] = the 24 B of block row i) to registers and the stage is
+// refilled with a later job's tile right away.
+__device__ __forceinline__ void stage_to_regs(const uint8_t* stage, int lane, uint2 (&v)[8][3]) {
+  const uint8_t* src = stage + (8 * (lane >> 3)) * (3 * kJobPx) + 24 * (lane & 7);
 #pragma unroll
-    for (int i = 0; i < 8; ++i)
+  for (int i = 0; i < 8; ++i)
 #pragma unroll
-      for (int k = 0; k < 3; ++k) v[i][k] = ldg64_first(p + i * a.rgb_pitch + 8 * k, pol);
-    return;
-  }
-  const int nb = 3 * min(8, max(0, a.w - x0));   // valid bytes of each row of the block
-#pragma unroll
-  for (int i = 0; i < 8; ++i) {
-    const bool rok = y0 + i < a.h;
-#pragma unroll
-    for (int k = 0; k < 3; ++k) {
-      uint2 t = make_uint2(0u, 0u);
-      if (rok && 8 * k + 8 <= nb) {
-        t = ldg64_first(p + (int64_t)i * a.rgb_pitch + 8 * k, pol);
-      } else if (rok && 8 * k < nb) {   // partial chunk at the right image edge: bytes
-        uint32_t b[8];
-#pragma unroll
-        for (int q = 0; q < 8; ++q) b[q] = 8 * k + q < nb ? p[(int64_t)i * a.rgb_pitch + 8 * k + q] : 0u;
-        t.x = b[0] | (b[1] << 8) | (b[2] << 16) | (b[3] << 24);
-        t.y = b[4] | (b[5] << 8) | (b[6] << 16) | (b[7] << 24);
-      }
-      v[i][k] = t;
-    }
-  }
+    for (int k = 0; k < 3; ++k) v[i][k] = *reinterpret_cast<const uint2*>(src + i * (3 * kJobPx) + 8 * k);
 }
 
 // Histogram increment at shared address `addr` (ATOMS.POPC.INC); the level
 // histograms are 1 KB-aligned, so bin b of level k is hb + 1024 k | 4 b.
 __device__ __forceinline__ void hadd(uint32_t addr) { asm volatile("red.shared.add.u32 [%0], 1;" ::"r"(addr) : "memory"); }
 
+// Level 0 gray into the slot (swizzled rows); level 1 only feeds the
+// histogram and level 2 (K3 re-derives it from level 0); levels 2..5 into
+// the slot.
 template <bool FULL>
 __device__ __forceinline__ void res_k1(const ResArgs& a, const uint2 (&v)[8][3], int jx, int jy, int lane,
                                        uint8_t* slot, uint32_t hb) {
@@ -216,8 +235,6 @@ __device__ __forceinline__ void res_k1(const ResArgs& a, const uint2 (&v)[8][3],
       if (FULL || (row_ok && 3 < nv1)) hadd((hb + 1024) | (s3 & 0x3fcu));
       const uint32_t x01 = (s0 + (s1 << 16)) >> 2, x23 = (s2 + (s3 << 16)) >> 2;
       l1[rp] = __byte_perm(x01, x23, 0x6420);
-      const int row1 = 4 * r + rp;
-      *reinterpret_cast<uint32_t*>(slot + l1_addr(row1, c >> 2) + 4 * (c & 3)) = l1[rp];
     }
   }
   if (a.n < 3) return;
@@ -265,16 +282,16 @@ __device__ __forceinline__ void res_k1(const ResArgs& a, const uint2 (&v)[8][3],
   }
 }
 
-// Zero the map words of image `img` that K3 ORs into (levels 2..5: a word
-// spans 2..16 jobs; its owner job, jx % 2^(k-1) == 0, clears it) and the
+// Zero the map words of image `img` that K3 ORs into (levels 4..5: a word
+// spans 8 / 16 jobs; its owner job, jx % 2^(k-1) == 0, clears it) and the
 // row-padding words past the last job column (levels 1..5), for this job's
 // rows.  Runs in K1(img); K3(img) starts only after the image's barrier.
 __device__ __forceinline__ void res_zero_words(const ResArgs& a, int img, int jx, int jy, int lane) {
   uint32_t* mtb = a.mtb + (int64_t)img * a.bit_img_words32;
   uint32_t* excl = a.excl + (int64_t)img * a.bit_img_words32;
-  if (lane < 15) {
-    const int k = lane < 8 ? 2 : lane < 12 ? 3 : lane < 14 ? 4 : 5;
-    const int row = lane - (k == 2 ? 0 : k == 3 ? 8 : k == 4 ? 12 : 14);
+  if (lane < 3) {   // levels 4 (2 rows) and 5 (1 row): OR targets
+    const int k = lane < 2 ? 4 : 5;
+    const int row = lane < 2 ? lane : 0;
     if (k < a.n && (jx & ((1 << (k - 1)) - 1)) == 0) {
       const int y = ((jy * kJobRows) >> k) + row;
       if (y < a.lh[k]) {
@@ -387,20 +404,45 @@ __device__ __forceinline__ void res_k3(const ResArgs& a, const RTh* th, uint32_t
     }
   }
   if (a.n < 2) return;
-  // ---- levels 1..5: lanes 0-15 level-1 rows (one word each), 16-23 level 2
-  //      (half words), 24-27 level 3 (bytes), 28-29 level 4, 30 level 5
-  const int k = lane < 16 ? 1 : lane < 24 ? 2 : lane < 28 ? 3 : lane < 30 ? 4 : lane < 31 ? 5 : 0;
-  const int row = lane - (k == 1 ? 0 : k == 2 ? 16 : k == 3 ? 24 : k == 4 ? 28 : 30);
+  // ---- level 1, derived from the slot's level 0 (pyramid.py:17-32, the same
+  //      nested rounding as K1): lane = (level-1 row lane >> 1, half lane & 1),
+  //      16 px from 2 x 32 level-0 px; the two halves of a word meet by shuffle
+  {
+    const int r1 = lane >> 1, hf = lane & 1;
+    const uint4 u0 = *reinterpret_cast<const uint4*>(slot + l0_addr(2 * r1, 2 * hf));
+    const uint4 u1 = *reinterpret_cast<const uint4*>(slot + l0_addr(2 * r1, 2 * hf + 1));
+    const uint4 d0 = *reinterpret_cast<const uint4*>(slot + l0_addr(2 * r1 + 1, 2 * hf));
+    const uint4 d1 = *reinterpret_cast<const uint4*>(slot + l0_addr(2 * r1 + 1, 2 * hf + 1));
+    const uint32_t uw[8] = {u0.x, u0.y, u0.z, u0.w, u1.x, u1.y, u1.z, u1.w};
+    const uint32_t dw[8] = {d0.x, d0.y, d0.z, d0.w, d1.x, d1.y, d1.z, d1.w};
+    uint32_t g[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+#pragma unroll
+    for (int m = 0; m < 4; ++m) {
+      const uint32_t xa = (box_sum(uw[2 * m], dw[2 * m], 0) + (box_sum(uw[2 * m], dw[2 * m], 1) << 16)) >> 2;
+      const uint32_t xb = (box_sum(uw[2 * m + 1], dw[2 * m + 1], 0) + (box_sum(uw[2 * m + 1], dw[2 * m + 1], 1) << 16)) >> 2;
+      g[m] = __byte_perm(xa, xb, 0x6420);
+    }
+    const int valid = min(16, a.lw[1] - (jx * (kJobPx / 2) + 16 * hf));
+    uint32_t m, e;
+    res_th_word(g, th[1], yt, ytl, valid, m, e);
+    const uint32_t mo = __shfl_xor_sync(0xffffffffu, m, 1), eo = __shfl_xor_sync(0xffffffffu, e, 1);
+    const int y = jy * (kJobRows / 2) + r1;
+    if (hf == 0 && y < a.lh[1]) {
+      const int64_t o = a.bit_off32[1] + (int64_t)y * a.nw32[1] + jx;
+      mtb[o] = m | (mo << 16);
+      excl[o] = e | (eo << 16);
+    }
+  }
+  if (a.n < 3) return;
+  // ---- levels 2..5 (OR-ed into words shared with neighbouring jobs): lanes
+  //      0-7 level-2 rows (16 px), 8-11 level 3 (8 px), 12-13 level 4, 14 level 5
+  const int k = lane < 8 ? 2 : lane < 12 ? 3 : lane < 14 ? 4 : lane < 15 ? 5 : 0;
+  const int row = lane - (k == 2 ? 0 : k == 3 ? 8 : k == 4 ? 12 : 14);
   if (k == 0 || k >= a.n) return;
   const int y = ((jy * kJobRows) >> k) + row;
   if (y >= a.lh[k]) return;
   uint32_t g[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-  if (k == 1) {
-    const uint4 q0 = *reinterpret_cast<const uint4*>(slot + l1_addr(row, 0));
-    const uint4 q1 = *reinterpret_cast<const uint4*>(slot + l1_addr(row, 1));
-    g[0] = q0.x; g[1] = q0.y; g[2] = q0.z; g[3] = q0.w;
-    g[4] = q1.x; g[5] = q1.y; g[6] = q1.z; g[7] = q1.w;
-  } else if (k == 2) {
+  if (k == 2) {
     const uint4 q0 = *reinterpret_cast<const uint4*>(slot + slot_off(2) + row * 16);
     g[0] = q0.x; g[1] = q0.y; g[2] = q0.z; g[3] = q0.w;
   } else if (k == 3) {
@@ -411,31 +453,50 @@ __device__ __forceinline__ void res_k3(const ResArgs& a, const RTh* th, uint32_t
   } else {
     g[0] = *reinterpret_cast<const unsigned short*>(slot + slot_off(5));
   }
-  const int npx = 64 >> k;                         // px of this level in the job's row
+  const int npx = kJobPx >> k;                     // px of this level in the job's row
   const int valid = min(npx, a.lw[k] - ((jx * kJobPx) >> k));
   uint32_t m, e;
   res_th_word(g, th[k], yt, ytl, valid, m, e);
-  const int64_t rowo = a.bit_off32[k] + (int64_t)y * a.nw32[k];
-  if (k == 1) {
-    mtb[rowo + jx] = m;
-    excl[rowo + jx] = e;
+  const int64_t o = a.bit_off32[k] + (int64_t)y * a.nw32[k] + (jx >> (k - 1));
+  const int part = jx & ((1 << (k - 1)) - 1);     // this job's part of the word
+  if (k <= 3) {
+    // levels 2 / 3: the job owns a half word / a byte of it (plain stores);
+    // the last job of a row also clears the parts of the word no job covers
+    const bool last = jx == a.jobs_x - 1;
+    if (k == 2) {
+      unsigned short* pm = reinterpret_cast<unsigned short*>(mtb + o) + part;
+      unsigned short* pe = reinterpret_cast<unsigned short*>(excl + o) + part;
+      pm[0] = (unsigned short)m;
+      pe[0] = (unsigned short)e;
+      if (last && part == 0) {
+        pm[1] = 0;
+        pe[1] = 0;
+      }
+    } else {
+      uint8_t* pm = reinterpret_cast<uint8_t*>(mtb + o);
+      uint8_t* pe = reinterpret_cast<uint8_t*>(excl + o);
+      pm[part] = (uint8_t)m;
+      pe[part] = (uint8_t)e;
+      if (last)
+        for (int b = part + 1; b < 4; ++b) {
+          pm[b] = 0;
+          pe[b] = 0;
+        }
+    }
   } else {
-    const int64_t o = rowo + (jx >> (k - 1));
-    const int sh = npx * (jx & ((1 << (k - 1)) - 1));
+    // levels 4 / 5: 4 / 2 bits per job, OR-ed into words cleared in K1
+    const int sh = npx * part;
     if (m) atomicOr(mtb + o, m << sh);
     if (e) atomicOr(excl + o, e << sh);
   }
 }
 
-// Lower median of one level's spread histogram (threshold.py:31-39).
-__device__ __forceinline__ int res_warp_median(const uint32_t* spread, int lane) {
-  uint32_t bins[8];
+// Lower median of one level's histogram (threshold.py:31-39): the smallest m
+// with cumsum[m] >= (total + 1) / 2.  One warp; lane owns bins 8 lane .. +7.
+__device__ __forceinline__ int res_warp_median(const uint32_t (&bins)[8], int lane) {
   uint32_t s = 0;
 #pragma unroll
-  for (int i = 0; i < 8; ++i) {
-    bins[i] = __ldcg(spread + (lane * 8 + i) * kHistStrideK1);
-    s += bins[i];
-  }
+  for (int i = 0; i < 8; ++i) s += bins[i];
   uint32_t incl = s;
 #pragma unroll
   for (int d = 1; d < 32; d <<= 1) {
@@ -450,59 +511,154 @@ __device__ __forceinline__ int res_warp_median(const uint32_t* spread, int lane)
   int med = 0;
   if (lane == L) {
     uint32_t cacc = incl - s;
+#pragma unroll
     for (int i = 0; i < 8; ++i) {
       cacc += bins[i];
-      if (cacc >= target) {
-        med = lane * 8 + i;
-        break;
-      }
+      if (cacc >= target && med == 0 && cacc - bins[i] < target) med = lane * 8 + i;
     }
   }
   return __shfl_sync(0xffffffffu, med, L);
 }
 
+// Histogram reduction without atomics (same-line REDs from 148 CTAs queue at
+// the L2 slice for tens of microseconds, and the median is on the critical
+// path here):
+//   1. the CTA that finishes its K1 jobs of image s stores its partial
+//      histograms (plain coalesced stores) into part[s & 1][cta], arrives on
+//      arrive[s]; the last to arrive raises every CTA's flag word 0;
+//   2. each CTA sums its ~10 bins over all partials into tot[s & 1], arrives
+//      on arrive2[s]; the last derives the n medians (threshold.py:31-39),
+//      writes them into every CTA's line (words 2..7) and raises word 1.
+// Per-CTA 128-B flag lines: no hot spot for the 148 pollers.
+__device__ __forceinline__ uint32_t* part_hist(const ResArgs& a, int s, int c) {
+  return a.part + ((int64_t)(s & 1) * gridDim.x + c) * (kRMaxLevels * 256);
+}
+
+__device__ __noinline__ void res_flush_hist(const ResArgs& a, int s, int lane, uint32_t hb) {
+  uint4* sh = reinterpret_cast<uint4*>(__cvta_shared_to_generic(hb));
+  uint4* dst = reinterpret_cast<uint4*>(part_hist(a, s, blockIdx.x));
+  for (int i = lane; i < a.n * 64; i += 32) {
+    dst[i] = sh[i];
+    sh[i] = make_uint4(0u, 0u, 0u, 0u);
+  }
+  __syncwarp();
+  int last = 0;
+  if (lane == 0) {
+    __threadfence();
+    last = r_atom_add_acqrel(a.arrive + s, 1u) == gridDim.x - 1;
+    RTRACE(a, s, 1);
+  }
+  last = __shfl_sync(0xffffffffu, last, 0);
+  if (!last) return;
+  __threadfence();
+  for (int c = lane; c < (int)gridDim.x; c += 32) r_st_relaxed(a.medflag + (int64_t)c * 32, (uint32_t)s + 1u);
+}
+
+// Phase 2 (the claimer warp of each CTA): this CTA's bins of the total, then
+// the medians (the last CTA).  Returns after the CTA's line holds them.
+__device__ __noinline__ void res_reduce_hist(const ResArgs& a, int s, int lane) {
+  const int G = gridDim.x, c = blockIdx.x;
+  uint32_t* line = a.medflag + (int64_t)c * 32;
+  if (lane == 0) {
+    while (r_ld_relaxed(line) < (uint32_t)s + 1u) __nanosleep(64);
+    RTRACE(a, s, 6);
+    r_fence_acquire();
+  }
+  __syncwarp();
+  const int nb = a.n * 256;
+  const int b0 = (int)((int64_t)c * nb / G), b1 = (int)((int64_t)(c + 1) * nb / G);
+  uint32_t* tot = a.tot + (int64_t)(s & 1) * (kRMaxLevels * 256);
+  for (int b = b0; b < b1; ++b) {
+    uint32_t v = 0;
+    for (int cc = lane; cc < G; cc += 32) v += __ldcg(part_hist(a, s, cc) + b);
+    v = warp_sum(v);
+    if (lane == 0) tot[b] = v;
+  }
+  __syncwarp();
+  int last = 0;
+  if (lane == 0) {
+    __threadfence();
+    last = r_atom_add_acqrel(a.arrive2 + s, 1u) == (uint32_t)G - 1;
+    RTRACE(a, s, 4);
+  }
+  last = __shfl_sync(0xffffffffu, last, 0);
+  if (last) {
+    uint32_t bins[kRMaxLevels][8];
+#pragma unroll
+    for (int k = 0; k < kRMaxLevels; ++k)
+#pragma unroll
+      for (int i = 0; i < 8; ++i) bins[k][i] = k < a.n ? __ldcg(tot + k * 256 + lane * 8 + i) : 0u;
+    int meds = 0;   // lane k holds level k's median
+#pragma unroll
+    for (int k = 0; k < kRMaxLevels; ++k) {
+      if (k >= a.n) break;
+      const int med = res_warp_median(bins[k], lane);
+      if (lane == k) meds = med;
+    }
+    if (lane < a.n) a.medians[(int64_t)s * a.n + lane] = meds;
+    uint32_t mk[kRMaxLevels];
+#pragma unroll
+    for (int k = 0; k < kRMaxLevels; ++k) mk[k] = (uint32_t)__shfl_sync(0xffffffffu, meds, k);
+    for (int cc = lane; cc < G; cc += 32)
+#pragma unroll
+      for (int k = 0; k < kRMaxLevels; ++k)
+        if (k < a.n) a.medflag[(int64_t)cc * 32 + 2 + k] = mk[k];
+    __syncwarp();
+    __threadfence();
+    for (int cc = lane; cc < G; cc += 32) r_st_relaxed(a.medflag + (int64_t)cc * 32 + 1, (uint32_t)s + 1u);
+    if (lane == 0) RTRACE(a, s, 5);
+  }
+  if (lane == 0) {
+    while (r_ld_relaxed(line + 1) < (uint32_t)s + 1u) __nanosleep(64);
+    r_fence_acquire();
+  }
+  __syncwarp();
+}
+
 // Threshold constants of image s in shared memory: the first warp that needs
-// them waits for every CTA's histogram flush and derives all n medians.
+// them waits for the CTA's flag (every CTA has flushed image s), sums the
+// histogram copies and derives all n medians (threshold.py:31-39); it also
+// clears this CTA's share of ring slot s + 2 (image s - 2's, read by every
+// CTA before image s could complete).
 __device__ __forceinline__ const RTh* res_need_medians(const ResArgs& a, ResShared& S, int s, int lane) {
   const int par = s & 1;
   const int want = s + 1, prev = s >= 2 ? s - 1 : 0;   // claims of one parity go s-2 -> s
-  volatile int* tag = &S.medtag[par];
   for (;;) {
-    if (*tag == want) break;
-    int role = 0;   // 0: not claimable yet (image s-2 unclaimed) or claimed by another warp
+    // role (decided by lane 0, warp-uniform): 2 = constants ready, 1 = this
+    // warp computes them, 0 = wait (claimed elsewhere, or image s-2 unclaimed)
+    int role = 0;
     if (lane == 0) {
-      const int cur = *reinterpret_cast<volatile int*>(&S.medclaim[par]);
-      if (cur == prev && atomicCAS(&S.medclaim[par], prev, want) == prev) role = 1;
+      if (r_ld_acquire_cta(&S.medtag[par]) == want) {
+        role = 2;
+      } else {
+        const int cur = *reinterpret_cast<volatile int*>(&S.medclaim[par]);
+        if (cur == prev && atomicCAS(&S.medclaim[par], prev, want) == prev) role = 1;
+      }
     }
     role = __shfl_sync(0xffffffffu, role, 0);
+    if (role == 2) break;
     if (role == 1) {
-      if (lane == 0)
-        while (r_ld_acquire(a.arrive + s) < gridDim.x) __nanosleep(64);
-      __syncwarp();
-      const uint32_t* gh = a.hist + (int64_t)s * a.hist_img_stride;
-      for (int k = 0; k < a.n; ++k) {
-        const int med = res_warp_median(gh + k * 256 * kHistStrideK1, lane);
-        if (lane == 0) {
-          RTh c;
-          c.med = (uint32_t)med * 0x01010101u;
-          c.ym = (uint32_t)(255 - med) * 0x01010101u;
-          c.yml = c.ym & 0x7f7f7f7fu;
-          c.med_lo = med <= 127;
-          S.th[par][k] = c;
-          if (blockIdx.x == 0) a.medians[(int64_t)s * a.n + k] = med;
-        }
+      res_reduce_hist(a, s, lane);
+      if (lane < a.n) {
+        const int med = (int)__ldcg(a.medflag + (int64_t)blockIdx.x * 32 + 2 + lane);
+        RTh c;
+        c.med = (uint32_t)med * 0x01010101u;
+        c.ym = (uint32_t)(255 - med) * 0x01010101u;
+        c.yml = c.ym & 0x7f7f7f7fu;
+        c.med_lo = med <= 127;
+        S.th[par][lane] = c;
       }
       __syncwarp();
       if (lane == 0) {
-        __threadfence_block();
-        *tag = want;
+        RTRACE(a, s, 2);
+        r_st_release_cta(&S.medtag[par], want);
       }
+      __syncwarp();
       break;
     }
-    __nanosleep(64);
+    __nanosleep(128);
   }
   __syncwarp();
-  __threadfence_block();
   return S.th[par];
 }
 
@@ -702,10 +858,13 @@ __device__ __forceinline__ void res_search_loop(const ResArgs& a, int lane) {
   int head = 0;
   while (head < total) {
     uint32_t it = 0;
-    if (lane == 0) it = r_ld_acquire(a.qitem + head);
+    if (lane == 0) {
+      it = r_ld_relaxed(a.qitem + head);
+      if (it) r_fence_acquire();
+    }
     it = __shfl_sync(0xffffffffu, it, 0);
     if (it == 0) {
-      __nanosleep(200);
+      __nanosleep(512);
       continue;
     }
     const int p = (int)((it - 1) >> 3), k = (int)((it - 1) & 7);
@@ -720,14 +879,35 @@ __device__ __forceinline__ void res_search_loop(const ResArgs& a, int lane) {
   }
 }
 
-__global__ void __launch_bounds__(kRThreads, 1) res_kernel(const __grid_constant__ ResArgs a) {
-  extern __shared__ __align__(128) uint8_t res_slots[];
+__global__ void __launch_bounds__(kRThreads, 1) res_kernel(const __grid_constant__ ResArgs a,
+                                                             const __grid_constant__ CUtensorMap rgb_map) {
+  extern __shared__ __align__(1024) uint8_t res_dyn[];   // [stages][kStageBytes] then [nc][kSlotBytes]
   __shared__ __align__(1024) uint32_t s_hist[6][256];   // this CTA's histograms of the image in K1
   __shared__ ResShared S;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int G = gridDim.x, c = blockIdx.x;
   const int j0 = (int)((int64_t)c * a.jobs / G);
   const int nc = (int)((int64_t)(c + 1) * a.jobs / G) - j0;   // jobs (= slots) of this CTA per image
+  const int nst = a.stages;
+  const int n_img = a.n_img;
+  uint8_t* stages = res_dyn;
+  uint8_t* slots = res_dyn + (size_t)nst * kStageBytes;
+  uint64_t pol;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+  // TMA tile copy of job q's RGB (q = s * nc + jl) into stage q % nst; one lane.
+  auto issue = [&](int q) {
+    const int s = q / nc, jl = q - s * nc;
+    if (s >= n_img) return;
+    if (a.img_ready && *reinterpret_cast<volatile int*>(&S.ready_img) < s) {   // streamed input: H2D landed
+      r_spin_geq(a.img_ready + s, 1u, 128);
+      atomicMax(&S.ready_img, s);
+    }
+    const int job = j0 + jl, jy = job / a.jobs_x, jx = job - jy * a.jobs_x;
+    const int st = q % nst;
+    *reinterpret_cast<volatile int*>(&S.stage_job[st]) = q;
+    mbar_expect_tx(&S.full[st], (uint32_t)kStageBytes);
+    tma_tile(stages + (size_t)st * kStageBytes, &rgb_map, (3 * kJobPx / 4) * jx, kJobRows * jy, s, &S.full[st], pol);
+  };
   for (int i = tid; i < 6 * 256; i += kRThreads) (&s_hist[0][0])[i] = 0u;
   if (tid < 2) {
     S.medtag[tid] = 0;
@@ -738,6 +918,13 @@ __global__ void __launch_bounds__(kRThreads, 1) res_kernel(const __grid_constant
   if (tid == 0) {
     S.claim = 0;
     S.ready_img = a.img_ready ? -1 : 0x7fffffff;
+    for (int st = 0; st < nst; ++st) {
+      mbar_init(&S.full[st], 1);
+      S.stage_job[st] = -1;
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    if (nc > 0)
+      for (int q = 0; q < nst; ++q) issue(q);
   }
   __syncthreads();
   if (warp >= kRK1Warps || nc == 0) {
@@ -745,32 +932,37 @@ __global__ void __launch_bounds__(kRThreads, 1) res_kernel(const __grid_constant
     return;
   }
   const uint32_t yt = (uint32_t)(255 - a.tol) * 0x01010101u, ytl = yt & 0x7f7f7f7fu;
-  uint64_t pol;
-  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
-  const int n_img = a.n_img;
+  const uint32_t hb = smem_addr(&s_hist[0][0]);
+  // Job sequence of this CTA: q = s * nc + jl for images s = 0..n_img-1, then
+  // the drain (s = n_img: K3 of the last image only).
   for (;;) {
-    int g = 0;
-    if (lane == 0) g = atomicAdd(&S.claim, 1);
-    g = __shfl_sync(0xffffffffu, g, 0);
-    const int s = g / nc, jl = g - s * nc;
+    int q = 0;
+    if (lane == 0) q = atomicAdd(&S.claim, 1);
+    q = __shfl_sync(0xffffffffu, q, 0);
+    const int s = q / nc, jl = q - s * nc;
     if (s > n_img) break;
     const int job = j0 + jl;
+#ifdef RES_EXP_TRACE
+    if (jl == 0 && lane == 0 && s < n_img) rtrace(a, s, 0);
+#endif
     const int jy = job / a.jobs_x, jx = job - jy * a.jobs_x;
     const bool full = (jx + 1) * kJobPx <= a.w && (jy + 1) * kJobRows <= a.h;
-    uint8_t* slot = res_slots + (size_t)jl * kSlotBytes;
+    uint8_t* slot = slots + (size_t)jl * kSlotBytes;
     uint2 v[8][3];
     if (s < n_img) {
-      if (s > *reinterpret_cast<volatile int*>(&S.ready_img)) {   // streamed input: wait for the H2D
-        if (lane == 0) {
-          while (r_ld_acquire(a.img_ready + s) == 0u) __nanosleep(128);
-          atomicMax(&S.ready_img, s);
-        }
-        __syncwarp();
+      // this job's RGB: wait for its stage, copy the block to registers,
+      // refill the stage with job q + nst
+      const int st = q % nst;
+      if (lane == 0)
+        while (*reinterpret_cast<volatile int*>(&S.stage_job[st]) != q) __nanosleep(20);
+      __syncwarp();
+      mbar_wait(&S.full[st], (uint32_t)(q / nst) & 1u);
+      stage_to_regs(stages + (size_t)st * kStageBytes, lane, v);
+      __syncwarp();
+      if (lane == 0) {
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        issue(q + nst);
       }
-      if (full)
-        res_load<true>(a, s, jx, jy, lane, v, pol);
-      else
-        res_load<false>(a, s, jx, jy, lane, v, pol);
     }
     if (s > 0) {
       // K3 of image s-1 out of this slot
@@ -782,40 +974,28 @@ __global__ void __launch_bounds__(kRThreads, 1) res_kernel(const __grid_constant
       last = __shfl_sync(0xffffffffu, last, 0);
       if (last && lane == 0) {
         S.k3cnt[(s - 1) & 1] = 0;
+        RTRACE(a, s - 1, 3);
         __threadfence();
         if (r_atom_add_acqrel(a.k3done + (s - 1), 1u) == (uint32_t)G - 1) {
           // every CTA wrote image s-1's maps: level n-1 of the pairs it completes
           const int p0 = __ldg(a.ready_start + (s - 1)), p1 = __ldg(a.ready_start + s);
-          for (int q = p0; q < p1; ++q) res_append(a, (uint32_t)(__ldg(a.ready_pairs + q) * 8 + (a.n - 1)) + 1u);
+          for (int qq = p0; qq < p1; ++qq) res_append(a, (uint32_t)(__ldg(a.ready_pairs + qq) * 8 + (a.n - 1)) + 1u);
         }
       }
     }
     if (s == n_img) continue;   // drain job: K3 only
     if (full)
-      res_k1<true>(a, v, jx, jy, lane, slot, smem_addr(&s_hist[0][0]));
+      res_k1<true>(a, v, jx, jy, lane, slot, hb);
     else
-      res_k1<false>(a, v, jx, jy, lane, slot, smem_addr(&s_hist[0][0]));
+      res_k1<false>(a, v, jx, jy, lane, slot, hb);
     res_zero_words(a, s, jx, jy, lane);
     __syncwarp();
     int last = 0;
     if (lane == 0) last = r_smem_add_acqrel(&S.k1cnt[s & 1], 1) == nc - 1;
     last = __shfl_sync(0xffffffffu, last, 0);
     if (last) {
-      // the CTA's histograms of image s are complete: flush, clear, arrive
-      uint32_t* gh = a.hist + (int64_t)s * a.hist_img_stride;
-      for (int i = lane; i < a.n * 256; i += 32) {
-        const uint32_t cnt = (&s_hist[0][0])[i];
-        if (cnt) {
-          atomicAdd(gh + (int64_t)i * kHistStrideK1, cnt);
-          (&s_hist[0][0])[i] = 0u;
-        }
-      }
-      __syncwarp();
-      if (lane == 0) {
-        S.k1cnt[s & 1] = 0;
-        __threadfence();
-        r_atom_add_acqrel(a.arrive + s, 1u);
-      }
+      if (lane == 0) S.k1cnt[s & 1] = 0;
+      res_flush_hist(a, s, lane, hb);
     }
   }
   res_search_loop(a, lane);
@@ -830,7 +1010,7 @@ __global__ void res_upload_kernel(int32_t* dst, int n, const __grid_constant__ R
   for (int i = threadIdx.x; i < n; i += blockDim.x) dst[i] = u.v[i];
 }
 
-int64_t spread_hist_elems(int n_levels);
+PFN_cuTensorMapEncodeTiled_v12000 k1_encode_tiled();
 
 }  // namespace mtb
 
@@ -839,21 +1019,32 @@ using namespace mtb;
 static int res_jobs(int w, int h) { return ((w + kJobPx - 1) / kJobPx) * ((h + kJobRows - 1) / kJobRows); }
 
 // Largest per-CTA job count the shared-memory slots hold.
-static int res_max_slots() { return (kRSmemLimit - (int)sizeof(ResShared) - 6 * 1024 - 1024) / kSlotBytes; }
+// Static shared memory of res_kernel (histograms + control) and the stage
+// ring depth that fits beside nc slots (0 if fewer than 3 stages fit).
+static int res_static_smem() { return 8 * 1024; }   // s_hist (6 KB, 1 KB-aligned) + ResShared, rounded up
+static int res_stages(int nc) {
+  const int room = kRSmemLimit - res_static_smem() - nc * kSlotBytes;
+  const int st = room / kStageBytes;
+  return st < 3 ? 0 : std::min(st, kRMaxStages);
+}
 
 extern "C" int mtb_resident_supported(int w, int h, int levels, int64_t rgb_pitch, int64_t rgb_img_stride) {
   Plan p;
   if (!make_plan(w, h, levels, &p) || p.n > kRMaxLevels) return 0;
-  if (rgb_pitch % 8 != 0 || rgb_img_stride % 8 != 0 || rgb_pitch < 3 * (int64_t)w) return 0;
+  // TMA: 16-B aligned rows and image strides; whole 16-px groups per row
+  if (w % 16 != 0 || rgb_pitch % 16 != 0 || rgb_img_stride % 16 != 0 || rgb_pitch < 3 * (int64_t)w) return 0;
+  if (k1_encode_tiled() == nullptr) return 0;
   const int jobs = res_jobs(w, h);
   const int per = (jobs + num_sms() - 1) / num_sms();
-  return per <= res_max_slots() ? 1 : 0;
+  return res_stages(per) > 0 ? 1 : 0;
 }
 
 extern "C" int64_t mtb_resident_sync_words(int n_img, int n_pairs, int levels) {
   const int64_t L = levels < 1 ? 1 : (levels > kRMaxLevels ? kRMaxLevels : levels);
-  // arrive, k3done [n_img]; qitem, qclaim [P*L]; qtail (+pad 31); pairs [2P]; ready_pairs [P]; ready_start [n_img+1]
-  return 2 * (int64_t)n_img + 2 * (int64_t)n_pairs * L + 32 + 3 * (int64_t)n_pairs + n_img + 1;
+  // part [2][G][1536]; tot [2][1536]; arrive, arrive2, k3done [n_img]; qitem, qclaim [P*L];
+  // qtail (+pad 31); medflag [G][32]; pairs [2P]; ready_pairs [P]; ready_start [n_img+1]
+  return 2 * (int64_t)num_sms() * 1536 + 2 * 1536 + 3 * (int64_t)n_img + 2 * (int64_t)n_pairs * L + 32 +
+         32 * (int64_t)num_sms() + 3 * (int64_t)n_pairs + n_img + 1;
 }
 
 static int res_upload(int32_t* dst, const std::vector<int32_t>& v, cudaStream_t st) {
@@ -903,8 +1094,6 @@ int mtb_resident_run(const uint8_t* rgb, int64_t rgb_pitch, int64_t rgb_img_stri
   a.n_img = n_img;
   a.mtb = reinterpret_cast<uint32_t*>(mtb);
   a.excl = reinterpret_cast<uint32_t*>(exclusion);
-  a.hist = hist_ws;
-  a.hist_img_stride = spread_hist_elems(p.n);
   a.medians = medians;
   a.n_pairs = n_pairs;
   a.acc = acc;
@@ -913,12 +1102,16 @@ int mtb_resident_run(const uint8_t* rgb, int64_t rgb_pitch, int64_t rgb_img_stri
   a.img_ready = img_ready;
   // sync_ws layout (mtb_resident_sync_words)
   uint32_t* w32 = sync_ws;
-  a.arrive = w32;
-  a.k3done = a.arrive + n_img;
+  a.part = w32;
+  a.tot = a.part + 2 * (int64_t)num_sms() * 1536;
+  a.arrive = a.tot + 2 * 1536;
+  a.arrive2 = a.arrive + n_img;
+  a.k3done = a.arrive2 + n_img;
   a.qitem = a.k3done + n_img;
   a.qclaim = a.qitem + (int64_t)n_pairs * p.n;
   a.qtail = a.qclaim + (int64_t)n_pairs * p.n;
-  int32_t* tab = reinterpret_cast<int32_t*>(a.qtail + 32);
+  a.medflag = a.qtail + 32;
+  int32_t* tab = reinterpret_cast<int32_t*>(a.medflag + 32 * (int64_t)num_sms());
   const int64_t zero_words = (int64_t)(tab - reinterpret_cast<int32_t*>(sync_ws));
   int32_t* d_pairs = tab;
   int32_t* d_ready = d_pairs + 2 * (int64_t)n_pairs;
@@ -942,7 +1135,6 @@ int mtb_resident_run(const uint8_t* rgb, int64_t rgb_pitch, int64_t rgb_img_stri
       tbl.push_back(q);
     }
   }
-  MTB_CUDA(cudaMemsetAsync(hist_ws, 0, sizeof(uint32_t) * spread_hist_elems(p.n) * n_img, st));
   if (n_pairs > 0) {
     MTB_CUDA(cudaMemsetAsync(errs, 0, sizeof(unsigned long long) * 9 * p.n * n_pairs, st));
     MTB_CUDA(cudaMemsetAsync(done, 0, sizeof(uint32_t) * p.n * n_pairs, st));
@@ -953,7 +1145,23 @@ int mtb_resident_run(const uint8_t* rgb, int64_t rgb_pitch, int64_t rgb_img_stri
 
   const int grid = std::min(num_sms(), a.jobs);   // every CTA owns >= 1 job (the barrier counts CTAs)
   const int nc = (a.jobs + grid - 1) / grid;
-  const int smem = nc * kSlotBytes;
+  a.stages = res_stages(nc);
+  MTB_REQUIRE(a.stages > 0, "image too large for the resident path");
+  const int smem = a.stages * kStageBytes + nc * kSlotBytes;
+  CUtensorMap map;
+  {
+    const cuuint64_t dims[3] = {(cuuint64_t)(3 * (int64_t)w / 4), (cuuint64_t)h, (cuuint64_t)n_img};
+    const cuuint64_t strides[2] = {(cuuint64_t)rgb_pitch, (cuuint64_t)rgb_img_stride};
+    const cuuint32_t box[3] = {3 * kJobPx / 4, kJobRows, 1};
+    const cuuint32_t estr[3] = {1, 1, 1};
+    const CUresult r = k1_encode_tiled()(&map, CU_TENSOR_MAP_DATA_TYPE_UINT32, 3, (void*)rgb, dims, strides, box,
+                                         estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                                         CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) {
+      set_error("cuTensorMapEncodeTiled failed for the RGB batch");
+      return MTB_ECUDA;
+    }
+  }
   MTB_CUDA(cudaFuncSetAttribute(res_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3((unsigned)grid);
@@ -965,10 +1173,34 @@ int mtb_resident_run(const uint8_t* rgb, int64_t rgb_pitch, int64_t rgb_img_stri
   attr[0].val.cooperative = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  const cudaError_t e = cudaLaunchKernelEx(&cfg, res_kernel, a);
+#ifdef RES_EXP_TRACE
+  const char* tpath = getenv("MTB_RES_TRACE");
+  const size_t tbytes = sizeof(unsigned long long) * 8 * (size_t)n_img * grid;
+  a.trace = nullptr;
+  if (tpath) {
+    MTB_CUDA(cudaMalloc(&a.trace, tbytes));
+    MTB_CUDA(cudaMemsetAsync(a.trace, 0, tbytes, st));
+  }
+#endif
+  const cudaError_t e = cudaLaunchKernelEx(&cfg, res_kernel, a, map);
   if (e != cudaSuccess) {
     set_error(std::string("res_kernel: ") + cudaGetErrorString(e));
     return MTB_ECUDA;
   }
+#ifdef RES_EXP_TRACE
+  if (tpath) {
+    std::vector<unsigned long long> h(tbytes / 8);
+    MTB_CUDA(cudaStreamSynchronize(st));
+    MTB_CUDA(cudaMemcpy(h.data(), a.trace, tbytes, cudaMemcpyDeviceToHost));
+    cudaFree(a.trace);
+    FILE* f = fopen(tpath, "wb");
+    if (f) {
+      const int hdr[2] = {n_img, grid};
+      fwrite(hdr, sizeof(int), 2, f);
+      fwrite(h.data(), 1, tbytes, f);
+      fclose(f);
+    }
+  }
+#endif
   return check_launch("res_kernel", 1);
 }
