@@ -22,19 +22,21 @@ int check_launch(const char* what, int n_launches) {
   return MTB_OK;
 }
 
-static int g_sms = 0;
+// SM count of the CURRENT device, cached per device ordinal.
+static std::atomic<int> g_sms[64];
 int num_sms() {
-  if (g_sms == 0) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    int v = 0;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (dev < 0 || dev >= 64) dev = 0;
+  int v = g_sms[dev].load(std::memory_order_relaxed);
+  if (v == 0) {
     if (cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || v <= 0) {
       cudaGetLastError();
       v = 148;
     }
-    g_sms = v;
+    g_sms[dev].store(v, std::memory_order_relaxed);
   }
-  return g_sms;
+  return v;
 }
 
 bool make_plan(int w, int h, int requested, Plan* p) {

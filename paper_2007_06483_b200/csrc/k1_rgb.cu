@@ -107,7 +107,7 @@ __global__ void __launch_bounds__(kK1Threads, 1) k1_rgb_pyramid_kernel(K1Args a,
       }
     }
   };
-  if (t == 0 && a.probe != 2) {
+  if (t == 0) {
     for (int s = 0; s < kK1Stages; ++s)
       if (t_begin + g + kK1Groups * s < t_end) issue(t_begin + g + kK1Groups * s, s);
   }
@@ -122,7 +122,7 @@ __global__ void __launch_bounds__(kK1Threads, 1) k1_rgb_pyramid_kernel(K1Args a,
     const bool full = (ty * kK1TileRows + kK1TileRows <= a.h) && (tx * kK1TilePx + kK1TilePx <= a.w);
     // Pull this thread's 8x8-pixel RGB block into registers.
     uint2 v[8][3];
-    if (a.probe != 2) mbar_wait(&S.full[g][stage], (uint32_t)(k / kK1Stages) & 1u);
+    mbar_wait(&S.full[g][stage], (uint32_t)(k / kK1Stages) & 1u);
     {
       const uint8_t* src = S.rgb[g][stage] + (8 * wg) * kK1RowBytes + 24 * lane;
 #pragma unroll
@@ -131,11 +131,10 @@ __global__ void __launch_bounds__(kK1Threads, 1) k1_rgb_pyramid_kernel(K1Args a,
         for (int c = 0; c < 3; ++c) v[r][c] = *reinterpret_cast<const uint2*>(src + r * kK1RowBytes + 8 * c);
     }
     group_bar(g);  // stage consumed by all 128 threads; l3 of tile k-1 complete
-    if (t == 0 && a.probe != 2 && tile + kK1Groups * kK1Stages < t_end) {
+    if (t == 0 && tile + kK1Groups * kK1Stages < t_end) {
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
       issue(tile + kK1Groups * kK1Stages, stage);
     }
-    if (a.probe == 1) continue;
     if (k > 0 && a.nl >= 5 && wg == ((k - 1) & 3))
       k1_levels45(a, gray, S.l3[g][(k - 1) & 1], ptx, pty, lane, hb, pfull, pol_gray);
     if (img != pimg) {
@@ -159,7 +158,7 @@ __global__ void __launch_bounds__(kK1Threads, 1) k1_rgb_pyramid_kernel(K1Args a,
     pfull = full;
   }
   group_bar(g);
-  if (a.probe != 1 && k > 0) {
+  if (k > 0) {
     if (a.nl >= 5 && wg == ((k - 1) & 3)) k1_levels45(a, gray, S.l3[g][(k - 1) & 1], ptx, pty, lane, hb, pfull, pol_gray);
     group_bar(g);
     flush(pimg);
@@ -212,10 +211,6 @@ int launch_k1_rgb(const uint8_t* rgb, int64_t rgb_pitch, int64_t rgb_img_stride,
   }
   a.hist_img_stride = hist_img_stride;
   a.keep_gray = g_keep_gray;
-  {
-    const char* pr = getenv("MTB_K1_PROBE");
-    a.probe = pr ? atoi(pr) : 0;
-  }
   a.tiles_x = (a.w + kK1TilePx - 1) / kK1TilePx;   // edge tiles included: TMA zero-fills outside the image
   a.tiles_y = (a.h + kK1TileRows - 1) / kK1TileRows;
   a.n_img = n_img;
@@ -225,11 +220,8 @@ int launch_k1_rgb(const uint8_t* rgb, int64_t rgb_pitch, int64_t rgb_img_stride,
     set_error("k1: too many tiles in one launch");
     return MTB_EINVAL;
   }
-  static bool attr_done = false;
-  if (!attr_done) {
-    MTB_CUDA(cudaFuncSetAttribute(k1_rgb_pyramid_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kK1SmemBytes));
-    attr_done = true;
-  }
+  // the shared-memory opt-in is per device (cheap; set on every call)
+  MTB_CUDA(cudaFuncSetAttribute(k1_rgb_pyramid_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kK1SmemBytes));
   int x = num_sms();
   if (x > (ntiles + kK1Groups - 1) / kK1Groups) x = (int)((ntiles + kK1Groups - 1) / kK1Groups);
   if (x < 1) x = 1;

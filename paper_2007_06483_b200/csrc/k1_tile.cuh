@@ -36,7 +36,6 @@ struct K1Args {
   int tiles_x, tiles_y;   // ceil(w/256) x ceil(h/32)
   int n_img;              // images of this launch (tiles are numbered image-major)
   int keep_gray;          // store gray with L2::evict_last (else evict_normal)
-  int probe;              // diagnostics (MTB_K1_PROBE): 1 = stream tiles only, 2 = compute only (no TMA)
 };
 
 __device__ __forceinline__ uint32_t smem_addr(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
@@ -71,17 +70,10 @@ __device__ __forceinline__ void group_bar(int g) {
   asm volatile("bar.sync %0, %1;" ::"r"(g + 1), "r"(kK1GroupThreads) : "memory");
 }
 // One histogram increment at a shared address (ATOMS.POPC.INC).
-#ifndef K1_EXP_NO_HIST
 __device__ __forceinline__ void hinc(uint32_t addr) { asm volatile("red.shared.add.u32 [%0], 1;" ::"r"(addr) : "memory"); }
-#else
-__device__ __forceinline__ void hinc(uint32_t addr) { asm volatile("" ::"r"(addr)); }
-#endif
 
 // Gray stores with an L2 policy (evict_last when a threshold pass follows).
 __device__ __forceinline__ void st_gray8(uint8_t* p, uint32_t a, uint32_t b, uint64_t policy) {
-#ifdef K1_EXP_NO_STORE
-  asm volatile("" ::"l"(p), "r"(a), "r"(b)); return;
-#endif
   asm volatile("st.global.L2::cache_hint.v2.u32 [%0], {%1, %2}, %3;" ::"l"(p), "r"(a), "r"(b), "l"(policy) : "memory");
 }
 __device__ __forceinline__ void st_gray4(uint8_t* p, uint32_t a, uint64_t policy) {
@@ -233,34 +225,21 @@ __host__ __device__ constexpr int tm_off(int k) {
 __host__ __device__ constexpr int tm_pitch(int k) { return 256 >> k; }
 constexpr int kTileGrayBytes = 11008;                                // 86 x 128 B
 
-// Tile-major gray stores.  With PIPE_GRAY_EVICT_LAST the level-0/1 stores
-// carry an L2::evict_last policy (the gray is read back one launch later).
-#ifdef PIPE_GRAY_EVICT_LAST
-#define TM_POL , uint64_t gpol
-#define TM_POLARG , gpol
+// Tile-major gray stores with an L2::evict_last policy (the gray is read
+// back one launch later).
 __device__ __forceinline__ void st8(uint8_t* p, uint32_t a, uint32_t b, uint64_t pol) {
   asm volatile("st.global.L2::cache_hint.v2.u32 [%0], {%1, %2}, %3;" ::"l"(p), "r"(a), "r"(b), "l"(pol) : "memory");
 }
-__device__ __forceinline__ void st4p(uint8_t* p, uint32_t a, uint64_t pol) {
-  asm volatile("st.global.L2::cache_hint.u32 [%0], %1, %2;" ::"l"(p), "r"(a), "l"(pol) : "memory");
-}
-#else
-#define TM_POL
-#define TM_POLARG
-__device__ __forceinline__ void st8(uint8_t* p, uint32_t a, uint32_t b) { *reinterpret_cast<uint2*>(p) = make_uint2(a, b); }
-__device__ __forceinline__ void st4p(uint8_t* p, uint32_t a) { *reinterpret_cast<uint32_t*>(p) = a; }
-#endif
 
 // k1_block for the tile-major layout: `tg` = this tile's gray region.
 template <bool FULL>
 __device__ __forceinline__ void k1_block_tm(const K1Args& a, uint8_t* tg, const uint2 (&v)[8][3], int tx, int ty,
-                                            int wg, int lane, uint32_t hb, uint8_t* l3_slot TM_POL) {
+                                            int wg, int lane, uint32_t hb, uint8_t* l3_slot, uint64_t gpol) {
   const int x0 = tx * kK1TilePx + 8 * lane;
   const int y0 = ty * kK1TileRows + 8 * wg;
   uint32_t l1[4];
   {
     uint8_t* p0 = tg + tm_off(0) + (8 * wg) * tm_pitch(0) + 8 * lane;
-    uint8_t* p1 = tg + tm_off(1) + (4 * wg) * tm_pitch(1) + 4 * lane;
     const int nv0 = FULL ? 8 : min(8, max(0, a.w - x0));
     const int nv1 = FULL ? 4 : min(4, max(0, a.lw[1] - (x0 >> 1)));
 #pragma unroll
@@ -278,7 +257,7 @@ __device__ __forceinline__ void k1_block_tm(const K1Args& a, uint8_t* tg, const 
           if (FULL || (row_ok && i < nv0)) hinc(hb | ((sa[i] >> 6) & 0x3fcu));
           if (FULL || (row_ok && 4 + i < nv0)) hinc(hb | ((sb[i] >> 6) & 0x3fcu));
         }
-        st8(p0 + r * tm_pitch(0), gw[j][0], gw[j][1] TM_POLARG);
+        st8(p0 + r * tm_pitch(0), gw[j][0], gw[j][1], gpol);
       }
       if (a.nl >= 2) {
         const uint32_t s0 = box_sum(gw[0][0], gw[1][0], 0), s1 = box_sum(gw[0][0], gw[1][0], 1);
@@ -291,9 +270,6 @@ __device__ __forceinline__ void k1_block_tm(const K1Args& a, uint8_t* tg, const 
         if (FULL || (row_ok && 3 < nv1)) hinc(hb1 | (s3 & 0x3fcu));
         const uint32_t x01 = (s0 + (s1 << 16)) >> 2, x23 = (s2 + (s3 << 16)) >> 2;
         l1[rp] = __byte_perm(x01, x23, 0x6420);
-#if defined(PIPE_L1_TASKS) && !defined(PIPE_PROBE_NO_L123)
-        st4p(p1 + rp * tm_pitch(1), l1[rp] TM_POLARG);   // else the level-0 threshold tasks derive level 1
-#endif
       }
     }
   }
@@ -311,9 +287,7 @@ __device__ __forceinline__ void k1_block_tm(const K1Args& a, uint8_t* tg, const 
       if (FULL || (row_ok && 0 < nv2)) hinc(hb2 | (s0 & 0x3fcu));
       if (FULL || (row_ok && 1 < nv2)) hinc(hb2 | (s1 & 0x3fcu));
       l2[r] = ((s0 >> 2) & 0xffu) | ((s1 << 6) & 0xff00u);
-#ifndef PIPE_PROBE_NO_L123
       *reinterpret_cast<unsigned short*>(p2 + r * tm_pitch(2)) = (unsigned short)l2[r];
-#endif
     }
   }
   if (a.nl < 4) return;

@@ -34,14 +34,8 @@
 #include <type_traits>
 #include <vector>
 
-// Level-0/1 gray is stored with L2::evict_last (no persisting set-aside: it
+// Level-0 gray is stored with L2::evict_last (no persisting set-aside: it
 // measured slower); the RGB stream is evict_first.
-#ifndef PIPE_GRAY_EVICT_NORMAL
-#ifndef PIPE_GRAY_EVICT_NORMAL
-#define PIPE_GRAY_EVICT_LAST
-#endif
-#endif
-
 #include "k1_tile.cuh"
 #include "swar.cuh"
 
@@ -49,14 +43,8 @@ namespace mtb {
 
 constexpr int kPipeMaxLevels = 6;
 constexpr int kPipeMaxItems = 96;
-#ifndef PIPE_THREADS
-#define PIPE_THREADS 512
-#endif
-constexpr int kPipeThreads = PIPE_THREADS;     // 12 K1 warps + 4 aux warps
-#ifndef PIPE_CTAS_PER_SM
-#define PIPE_CTAS_PER_SM 1
-#endif
-constexpr int kPipeCtasPerSm = PIPE_CTAS_PER_SM;   // 2: consecutive launches share an SM (PDL overlap)
+constexpr int kPipeThreads = 512;     // 12 K1 warps + 4 aux warps
+constexpr int kPipeCtasPerSm = 1;
 constexpr int kPipeWarps = kPipeThreads / 32;
 constexpr int kK3Units = 4;                     // K3 task = 4 x 32 bitmap words = 4 KB of gray
 constexpr int kK3Words = 32 * kK3Units;
@@ -93,14 +81,12 @@ struct PipeArgs {
   const uint32_t* img_ready;         // [img] nonzero once the image's RGB is in HBM (streamed input), or null
   uint32_t* decided;                 // [P][n] 1 once the (pair, level) offset is published
   int n_launch;
-  int probe;                         // diagnostics (MTB_PIPE_PROBE): 1 = no K1 tiles, 2 = no aux tasks
   int j;                             // this launch's index
   int k1_img0, k1_cnt;               // images k1_img0 .. +k1_cnt-1 of the K1 part (k1_cnt may be 0)
   int gray_slots;                    // gray ring slots in use: 3 x images per launch
   int th_img0, th_cnt;               // images of the K3 part
   int n_items;
   int search_tiles;
-  unsigned long long* trace;         // optional [launch][cta][8] %globaltimer stamps (diagnostics)                  // total search warp-tiles of this launch
   PipeItem items[kPipeMaxItems];
 };
 
@@ -115,20 +101,11 @@ struct ThConst {
 // Warp roles: warps 0..7 = two K1 groups streaming image j (never wait on
 // earlier launches: the gray ring has 3 slots), warps 8..15 = the aux warps
 // (K3 + search) which wait for launch j-1.
-#ifndef PIPE_K1_GROUPS
-#define PIPE_K1_GROUPS 3
-#endif
-#ifndef PIPE_STAGES
-#define PIPE_STAGES 2
-#endif
-constexpr int kPK1Groups = PIPE_K1_GROUPS;
+constexpr int kPK1Groups = 3;
 constexpr int kPK1Warps = 4 * kPK1Groups;
 constexpr int kPAuxWarps = kPipeWarps - kPK1Warps;
-constexpr int kPStages = PIPE_STAGES;
-#ifndef PIPE_IMGS
-#define PIPE_IMGS 2
-#endif
-constexpr int kPipeImgs = PIPE_IMGS;          // images per launch (K1 part and K3 part)
+constexpr int kPStages = 2;
+constexpr int kPipeImgs = 2;                  // images per launch (K1 part and K3 part)
 constexpr int kPGraySlots = 3 * kPipeImgs;    // gray ring capacity: written, being read, lagging readers
                                               // (3 x images per launch slots in use)
 constexpr int kAuxPhases = 7;     // aux task phases: K3 levels 0..3, levels 4..5, padding, search
@@ -172,40 +149,26 @@ __device__ __forceinline__ void grid_dep_launch() { asm volatile("griddepcontrol
 // CTAs are all resident once its successor runs (a launch can only start
 // after every CTA of its predecessor has started), so spinning cannot
 // deadlock.
-__device__ __forceinline__ uint32_t ld_acquire(const uint32_t* p) {
+__device__ __forceinline__ uint32_t ld_relaxed(const uint32_t* p) {
   uint32_t v;
-  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
   return v;
 }
+// Poll with relaxed loads and acquire once the value is reached: an acquire
+// load at gpu scope invalidates the SM's L1 (CCTL.IVALL) on every poll.
+// MTB_SPIN_LIMIT (debug builds) bounds the spin: a lost flag then fails the
+// launch (trap) instead of hanging the GPU.
 __device__ __forceinline__ void spin_geq(const uint32_t* p, uint32_t v) {
-#ifndef PIPE_SPIN_NS
-#define PIPE_SPIN_NS 100
-#endif
-  while (ld_acquire(p) < v) __nanosleep(PIPE_SPIN_NS);
-}
-
-// Diagnostics (MTB_PIPE_TRACE): kTraceWords u64 per (launch, CTA).
-//  0..7 stamps, 8+p first task of aux phase p, 16 %smid, 17 entry, 18 exit,
-//  19/20/22 ns spun on search / threshold / gray-slot dependencies,
-//  21 first K1 tile ready, 24+w end of warp w's aux drain, 40+w / 56+w start
-//  and phase of the last task warp w claimed.
-constexpr int kTraceWords = 80;
-__device__ __forceinline__ unsigned long long gtime() {
-  unsigned long long t;
-  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
-  return t;
-}
-__device__ __forceinline__ void spin_geq_traced(unsigned long long* trace, int slot, const uint32_t* p, uint32_t v) {
-  if (!trace) {
-    spin_geq(p, v);
-    return;
+#ifdef MTB_SPIN_LIMIT
+  long long n = 0;
+  while (ld_relaxed(p) < v) {
+    __nanosleep(100);
+    if (++n > (long long)MTB_SPIN_LIMIT) __trap();
   }
-  const unsigned long long t0 = gtime();
-  spin_geq(p, v);
-  atomicAdd(trace + slot, gtime() - t0);
-}
-__device__ __forceinline__ unsigned long long* trace_rec(const PipeArgs& a) {
-  return a.trace ? a.trace + ((int64_t)a.j * gridDim.x + blockIdx.x) * kTraceWords : nullptr;
+#else
+  while (ld_relaxed(p) < v) __nanosleep(100);
+#endif
+  asm volatile("fence.acq_rel.gpu;" ::: "memory");
 }
 
 // Lower median of one level's spread histogram (threshold.py:31-39): the
@@ -463,7 +426,6 @@ __device__ __forceinline__ void k3_bulk_units_l0(const PipeArgs& a, uint32_t* mt
   }
 }
 
-#ifndef PIPE_L1_TASKS
 // Level 1 of a level-0 task's half tile, derived from its staged level-0
 // rows (pyramid.py:17-32, the same rounding as K1's level 1, so the bits
 // match the median K1's level-1 histogram gave): 16 x 256 px -> 8 x 128 px =
@@ -496,7 +458,6 @@ __device__ __forceinline__ void k3_level1_from_l0(const PipeArgs& a, uint32_t* m
     excl[o] = e;
   }
 }
-#endif
 
 __device__ __forceinline__ void k3_bulk_finish(const PipeArgs& a, const uint8_t* slot, uint32_t* mtb, uint32_t* excl,
                                                const ThConst* th, uint32_t yt, uint32_t ytl, int K, int r, int lane,
@@ -534,9 +495,7 @@ __device__ __forceinline__ void k3_bulk_finish(const PipeArgs& a, const uint8_t*
   } else {
     k3_bulk_units<false>(a, mtb, excl, c, yt, ytl, K, r, lane, buf);
   }
-#ifndef PIPE_L1_TASKS
   if (K == 0 && a.n > 1) k3_level1_from_l0(a, mtb, excl, th[1], yt, ytl, r, lane, buf);
-#endif
   const int lwpt = 8 - 2 * K, wpt = 1 << lwpt;
   const int ntiles = a.g.tiles_x * a.g.tiles_y;
   // line `lane` of the task's gray: drop it from L2 without write-back
@@ -604,10 +563,10 @@ __device__ __forceinline__ void pipe_search_tile(const PipeArgs& a, const PipeIt
   const int n = a.n;
   if (lane == 0) {
     if (k + 1 < n) {
-      spin_geq_traced(trace_rec(a), 19, a.decided + (int64_t)it.pair * n + (k + 1), 1u);
+      spin_geq(a.decided + (int64_t)it.pair * n + (k + 1), 1u);
     } else {
-      spin_geq_traced(trace_rec(a), 19, a.k3_done + it.ref, gridDim.x);
-      spin_geq_traced(trace_rec(a), 19, a.k3_done + it.tgt, gridDim.x);
+      spin_geq(a.k3_done + it.ref, gridDim.x);
+      spin_geq(a.k3_done + it.tgt, gridDim.x);
     }
   }
   __syncwarp();
@@ -783,7 +742,6 @@ struct AuxCtx {
   SearchStage* stage;          // search staging (aliases kbuf)
   uint8_t* kbuf;               // 2 x 4 KB K3 staging
   unsigned long long* kbar;    // its 2 mbarriers
-  bool tracer;   // diagnostics: this warp stamps phase starts (MTB_PIPE_TRACE)
 };
 
 __device__ __forceinline__ void named_bar(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory"); }
@@ -793,17 +751,9 @@ __device__ __forceinline__ int aux_phase_tasks1(const PipeArgs& a, int p) {
   const bool th = a.th_cnt > 0;
   switch (p) {
     case 0: return th ? (th_level_units<0>(a) + kK3Units - 1) / kK3Units : 0;
-#ifdef PIPE_PROBE_NO_L123   // diagnostics only (wrong maps): no level 1-3 gray stores / thresholds
-    case 1: case 2: case 3: return 0;
-#elif !defined(PIPE_L1_TASKS)
     case 1: return 0;   // level 1 is derived inside the level-0 tasks
     case 2: return th && a.n > 2 ? (th_level_units<2>(a) + kK3Units - 1) / kK3Units : 0;
     case 3: return th && a.n > 3 ? (th_level_units<3>(a) + kK3Units - 1) / kK3Units : 0;
-#else
-    case 1: return th && a.n > 1 ? (th_level_units<1>(a) + kK3Units - 1) / kK3Units : 0;
-    case 2: return th && a.n > 2 ? (th_level_units<2>(a) + kK3Units - 1) / kK3Units : 0;
-    case 3: return th && a.n > 3 ? (th_level_units<3>(a) + kK3Units - 1) / kK3Units : 0;
-#endif
     case 4: return th ? a.th_units0[a.n] - a.th_units0[a.n < 4 ? a.n : 4] : 0;
     case 5: return th ? (a.th_pad_words + 31) / 32 : 0;
     default: return a.search_tiles;   // 6
@@ -875,17 +825,11 @@ __device__ __forceinline__ void aux_run(const PipeArgs& a, PipeSmem& S, const Au
 // Queue order q -> phase: search tiles first (their CTA partial counts are
 // flushed per item as soon as the CTA's last tile of it is done, so the next
 // launch's level can start early), then K3 levels 3, 2, 0 (+1), [1: no tasks],
-// 4..5, padding (PIPE_K3_ORDER; PIPE_SEARCH_Q moves the search tiles).
-#ifndef PIPE_SEARCH_Q
-#define PIPE_SEARCH_Q 0
-#endif
-constexpr int kSearchQ = PIPE_SEARCH_Q;   // queue position of the search tiles
-#ifndef PIPE_K3_ORDER
-#define PIPE_K3_ORDER 1
-#endif
+// 4..5, padding.
+constexpr int kSearchQ = 0;   // queue position of the search tiles
 __device__ __forceinline__ int aux_phase_of(const PipeArgs& a, int q) {
   const int k = q == kSearchQ ? 6 : (q < kSearchQ ? q : q - 1);
-  if (PIPE_K3_ORDER == 1 && k < 4) {
+  if (k < 4) {
     // the latency-bound gathered levels 3 and 2 first, level 0 (with level 1
     // derived in it) last, so the CTA's final tasks are the cheap contiguous
     // ones (+0.8 % at 24 MP, +0.2 % at 12 MP)
@@ -893,14 +837,6 @@ __device__ __forceinline__ int aux_phase_of(const PipeArgs& a, int q) {
     return k == 0 ? order[0] : (k == 1 ? order[1] : (k == 2 ? order[2] : order[3]));
   }
   return k;
-}
-
-__device__ __forceinline__ void aux_stamp(const PipeArgs& a, int i) {
-  if (a.trace) {
-    unsigned long long t;
-    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
-    a.trace[((int64_t)a.j * gridDim.x + blockIdx.x) * kTraceWords + i] = t;
-  }
 }
 
 // The threshold constants of image th_img are needed only by K3 and level
@@ -914,7 +850,7 @@ __device__ __forceinline__ void aux_need_thresholds(const PipeArgs& a, PipeSmem&
   if (lane == 0) claim = atomicCAS(&S.th_state, 0, 1) == 0;
   claim = __shfl_sync(0xffffffffu, claim, 0);
   if (claim) {
-    if (lane < a.th_cnt) spin_geq_traced(trace_rec(a), 20, a.med_ready + a.th_img0 + lane, 1u);
+    if (lane < a.th_cnt) spin_geq(a.med_ready + a.th_img0 + lane, 1u);
     __syncwarp();
     if (lane < a.n * a.th_cnt) {
       const int b = lane / a.n, k = lane - b * a.n;
@@ -928,10 +864,7 @@ __device__ __forceinline__ void aux_need_thresholds(const PipeArgs& a, PipeSmem&
     }
     __threadfence_block();
     __syncwarp();
-    if (lane == 0) {
-      *st = 2;
-      aux_stamp(a, 5);
-    }
+    if (lane == 0) *st = 2;
   } else {
     while (*st != 2) __nanosleep(32);
   }
@@ -978,18 +911,6 @@ __device__ __forceinline__ void aux_drain(const PipeArgs& a, PipeSmem& S, const 
         r -= t1;
         ++bi;
       }
-    if (a.trace && p >= 0 && x.lane == 0) {   // last task claimed by this warp: start, phase
-      trace_rec(a)[40 + (threadIdx.x >> 5)] = gtime();
-      trace_rec(a)[56 + (threadIdx.x >> 5)] = p;
-    }
-    if (a.trace && p >= 0 && x.tracer && x.lane == 0) {
-      unsigned long long* slot = a.trace + ((int64_t)a.j * gridDim.x + blockIdx.x) * kTraceWords + 8 + p;
-      if (*slot == 0) {
-        unsigned long long tt;
-        asm volatile("mov.u64 %0, %globaltimer;" : "=l"(tt));
-        *slot = tt;
-      }
-    }
     const bool k3 = p >= 0 && p < 4;
     if (k3) aux_need_thresholds(a, S, x.lane);
     if (k3) k3_bulk_issue(a, aux_slot(a, bi), p, r, x.lane, x.kbuf + nb * kK3Bytes, &x.kbar[nb]);
@@ -1071,15 +992,6 @@ __global__ void __launch_bounds__(kPipeThreads, kPipeCtasPerSm) pipe_kernel(cons
   const int tid = threadIdx.x;
   const int lane = tid & 31;
   const int warp = tid >> 5;
-  if (a.trace && threadIdx.x == 0) {   // diagnostics: SM and entry time of this CTA
-    unsigned long long t;
-    uint32_t sm;
-    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
-    asm volatile("mov.u32 %0, %smid;" : "=r"(sm));
-    unsigned long long* tr = a.trace + ((int64_t)a.j * gridDim.x + blockIdx.x) * kTraceWords;
-    tr[16] = sm;
-    tr[17] = t;
-  }
   // All dependencies on earlier launches are explicit flags, so the next
   // launch may be scheduled as soon as this one's CTAs are all resident.
   grid_dep_launch();
@@ -1089,13 +1001,6 @@ __global__ void __launch_bounds__(kPipeThreads, kPipeCtasPerSm) pipe_kernel(cons
     S.th_state = 0;
   }
   __syncthreads();
-  auto stamp = [&](int i) {
-    if (a.trace && (tid == 0 || tid == 32 * kPK1Warps)) {
-      unsigned long long t;
-      asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
-      a.trace[((int64_t)a.j * gridDim.x + blockIdx.x) * kTraceWords + i] = t;
-    }
-  };
 
   if (warp < kPK1Warps) {
     // ======================= K1 warps: image k1_img ==========================
@@ -1104,17 +1009,14 @@ __global__ void __launch_bounds__(kPipeThreads, kPipeCtasPerSm) pipe_kernel(cons
     const int wg = warp & 3;
     const int kt = tid;               // 0..255 among the K1 threads
     const uint32_t hb = smem_addr(&S.hist[0][0]);
-    stamp(0);
     if (a.k1_cnt > 0) {
       const int tiles_img = a.g.tiles_x * a.g.tiles_y;
-      const int tiles_all = a.probe == 1 ? 0 : a.k1_cnt * tiles_img;   // probe 1: no tiles, still publish
+      const int tiles_all = a.k1_cnt * tiles_img;
       uint32_t* ctr = a.ctr + a.j;   // K1 tile counter of this launch
       uint64_t pol_first;
       asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol_first));
-#ifdef PIPE_GRAY_EVICT_LAST
       uint64_t gpol;
       asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(gpol));
-#endif
       for (int i = kt; i < kPipeImgs * 6 * 256; i += 32 * kPK1Warps) (&S.hist[0][0][0])[i] = 0;
       // Claim the next tile for ring stage `stage` (launch-wide counter over
       // the k1_cnt images' tiles, image-major: CTAs that start late take
@@ -1151,7 +1053,7 @@ __global__ void __launch_bounds__(kPipeThreads, kPipeCtasPerSm) pipe_kernel(cons
       // gray slot i % kPGraySlots last held image i - kPGraySlots: wait until
       // every CTA has thresholded it
       if (kt < a.k1_cnt && a.k1_img0 + kt >= a.gray_slots)
-        spin_geq_traced(trace_rec(a), 22, a.k3_done + (a.k1_img0 + kt - a.gray_slots), gridDim.x);
+        spin_geq(a.k3_done + (a.k1_img0 + kt - a.gray_slots), gridDim.x);
       named_bar(5, 32 * kPK1Warps);   // hist zeroed, mbarriers initialised, slots free
       int k = 0, ptx = 0, pty = 0;
       uint8_t* ptg = nullptr;
@@ -1160,7 +1062,6 @@ __global__ void __launch_bounds__(kPipeThreads, kPipeCtasPerSm) pipe_kernel(cons
       for (;; ++k) {
         const int stage = k % kPStages;
         mbar_wait(&S.full[g][stage], (uint32_t)(k / kPStages) & 1u);
-        if (k == 0 && t == 0 && g == 0 && a.trace) trace_rec(a)[21] = gtime();
         int tile = *reinterpret_cast<volatile int*>(&S.tile_of[g][stage]);
         if (tile < 0) break;
         int b = 0;
@@ -1190,9 +1091,9 @@ __global__ void __launch_bounds__(kPipeThreads, kPipeCtasPerSm) pipe_kernel(cons
         const uint32_t hbi = hb + (uint32_t)b * (6 * 256 * 4);
         uint8_t* l3_slot = &S.l3[g][k & 1][wg][lane];
         if (full)
-          k1_block_tm<true>(a.g, tg, v, tx, ty, wg, lane, hbi, l3_slot TM_POLARG);
+          k1_block_tm<true>(a.g, tg, v, tx, ty, wg, lane, hbi, l3_slot, gpol);
         else
-          k1_block_tm<false>(a.g, tg, v, tx, ty, wg, lane, hbi, l3_slot TM_POLARG);
+          k1_block_tm<false>(a.g, tg, v, tx, ty, wg, lane, hbi, l3_slot, gpol);
         ptx = tx;
         pty = ty;
         ptg = tg;
@@ -1206,7 +1107,6 @@ __global__ void __launch_bounds__(kPipeThreads, kPipeCtasPerSm) pipe_kernel(cons
       // for each image of which this is the last CTA it also publishes the
       // medians (threshold.py:31-39).  Counter: word 1 of bin 0's 128-B line.
       // The other K1 warps go straight to the aux work.
-      stamp(1);
       int mine = 0;
       if (lane == 0) {
         __threadfence_block();
@@ -1240,7 +1140,6 @@ __global__ void __launch_bounds__(kPipeThreads, kPipeCtasPerSm) pipe_kernel(cons
             }
           }
         }
-        stamp(2);
       }
     }
     // Join the aux work (the aux prologue has long finished: spin on its flag).
@@ -1271,16 +1170,12 @@ __global__ void __launch_bounds__(kPipeThreads, kPipeCtasPerSm) pipe_kernel(cons
                 : &S.abuf[warp - kPK1Warps][0][0];
   ax.kbar = S.kbar[warp];
   ax.stage = reinterpret_cast<SearchStage*>(ax.kbuf);
-  ax.tracer = true;
-  if (a.probe != 2) aux_drain(a, S, ax);
-  stamp(warp < kPK1Warps ? 3 : 5);
-  if (a.trace && lane == 0) trace_rec(a)[24 + warp] = gtime();
+  aux_drain(a, S, ax);
   named_bar(10, kPipeThreads);   // every task of this CTA done
   if (tid == 0 && a.th_cnt > 0) {
     __threadfence();
     for (int b = 0; b < a.th_cnt; ++b) atomicAdd(a.k3_done + a.th_img0 + b, 1u);
   }
-  if (a.trace && tid == 0) trace_rec(a)[18] = gtime();
 
 }
 
@@ -1294,10 +1189,8 @@ using namespace mtb;
 
 // Images per launch: 2 up to 64 MB of gray per image (24 MP = 33 MB: 2
 // images per launch measured 16.7 K vs 16.1 K pairs/s although more gray
-// spills to HBM; 12 MP: 28.2 K vs 24.1 K), else 1.  MTB_PIPE_IMGS overrides.
+// spills to HBM; 12 MP: 28.2 K vs 24.1 K), else 1.
 static int pipe_images_per_launch(int w, int h) {
-  const char* e = getenv("MTB_PIPE_IMGS");
-  if (e) return std::max(1, std::min(kPipeImgs, atoi(e)));
   const int64_t slot = (int64_t)((w + kK1TilePx - 1) / kK1TilePx) * ((h + kK1TileRows - 1) / kK1TileRows) *
                        kTileGrayBytes;
   return slot <= ((int64_t)64 << 20) ? kPipeImgs : 1;
@@ -1306,56 +1199,51 @@ static int pipe_images_per_launch(int w, int h) {
 extern "C" int mtb_align_fused_images_per_launch(int w, int h) { return pipe_images_per_launch(w, h); }
 
 // Launch plan of one mtb_align_fused call: launch j runs K1 of images
-// jB .. jB+B-1 and K3 of images (j-1)B .. jB-1; pair q runs level
-// n-1-(j-t(q)) in launch j, t(q) = max(ref, tgt) / B + 2 (the launch after
-// its images' K3).  After the last K3 launch only search levels remain:
-// with MTB_PIPE_MERGE=1 they run in ONE launch whose items go coarse to
-// fine (each item's tiles wait for the previous level's decided flag, which
-// every CTA's per-item flush releases) - measured 6 % slower per 32-pair
-// step than one launch per level, so off by default.
+// jB .. jB+B-1 and K3 of images (j-1)B .. jB-1; pair q runs its levels
+// n-1 .. 0 in launches t(q) .. t(q)+n-1, t(q) >= max(ref, tgt) / B + 2 (the
+// launch after its images' K3).  A launch carries at most kPipeMaxItems
+// (pair, level) items: a pair whose levels would overfill one of its launches
+// starts later (greedy, pairs in readiness order), so the whole plan is valid
+// before anything is enqueued.  (One launch for all trailing levels, chained
+// through the decided flags, measured 6 % slower than one launch per level.)
 struct PipeLaunch {
   int j;                                    // launch index (K1/K3 images, tile counter)
   std::vector<std::pair<int, int>> items;   // (pair, level)
 };
 static std::vector<PipeLaunch> pipe_plan(int n_img, int B, int nl, const int32_t* pairs, int n_pairs) {
   const int k1_launches = (n_img + B - 1) / B;
-  std::vector<int> ready(n_pairs);
-  int J = k1_launches + 1;
+  std::vector<int> order(n_pairs), start(n_pairs);
   for (int q = 0; q < n_pairs; ++q) {
-    const int r = pairs[2 * q], tg = pairs[2 * q + 1];
-    ready[q] = (r > tg ? r : tg) / B + 2;
-    J = std::max(J, ready[q] + nl);
+    order[q] = q;
+    start[q] = std::max(pairs[2 * q], pairs[2 * q + 1]) / B + 2;
   }
-  const int jm = k1_launches + 1;   // first launch without K1 / K3 work
-  std::vector<PipeLaunch> plan;
-  for (int j = 0; j < std::min(J, jm); ++j) {
-    PipeLaunch l{j, {}};
-    for (int q = 0; q < n_pairs; ++q) {
-      const int d = j - ready[q];
-      if (d >= 0 && d < nl) l.items.emplace_back(q, nl - 1 - d);
+  std::stable_sort(order.begin(), order.end(), [&](int x, int y) { return start[x] < start[y]; });
+  std::vector<int> load;   // items per launch
+  int J = k1_launches + 1;
+  for (int q : order) {
+    int t = start[q];
+    for (;;) {
+      if ((int)load.size() < t + nl) load.resize(t + nl, 0);
+      bool fits = true;
+      for (int d = 0; d < nl && fits; ++d) fits = load[t + d] < kPipeMaxItems;
+      if (fits) break;
+      ++t;
     }
-    plan.push_back(std::move(l));
+    for (int d = 0; d < nl; ++d) ++load[t + d];
+    start[q] = t;
+    J = std::max(J, t + nl);
   }
-  if (J > jm) {
-    PipeLaunch m{jm, {}};
-    for (int lev = nl - 1; lev >= 0; --lev)
-      for (int q = 0; q < n_pairs; ++q)
-        if (ready[q] + (nl - 1 - lev) >= jm) m.items.emplace_back(q, lev);
-    const char* mg = getenv("MTB_PIPE_MERGE");
-    if ((int)m.items.size() <= kPipeMaxItems && mg && atoi(mg)) {
-      plan.push_back(std::move(m));
-    } else {
-      for (int j = jm; j < J; ++j) {
-        PipeLaunch l{j, {}};
-        for (int q = 0; q < n_pairs; ++q) {
-          const int d = j - ready[q];
-          if (d >= 0 && d < nl) l.items.emplace_back(q, nl - 1 - d);
-        }
-        plan.push_back(std::move(l));
-      }
-    }
-  }
+  std::vector<PipeLaunch> plan(J);
+  for (int j = 0; j < J; ++j) plan[j].j = j;
+  for (int q : order)
+    for (int d = 0; d < nl; ++d) plan[start[q] + d].items.emplace_back(q, nl - 1 - d);
   return plan;
+}
+
+// Upper bound of the launch count (sizes the per-launch tile counters).
+static int64_t pipe_max_launches(int n_img, int n_pairs, int levels) {
+  const int64_t L = levels < 1 ? 1 : levels;
+  return (int64_t)n_img + 8 + ((int64_t)n_pairs * L + kPipeMaxItems - 1) / kPipeMaxItems + L;
 }
 
 extern "C" int mtb_align_fused_launches(int w, int h, int levels, int n_img, const int32_t* pairs_host, int n_pairs) {
@@ -1364,16 +1252,8 @@ extern "C" int mtb_align_fused_launches(int w, int h, int levels, int n_img, con
   return (int)pipe_plan(n_img, pipe_images_per_launch(w, h), p.n, pairs_host, n_pairs).size();
 }
 
-extern "C" int64_t mtb_resident_sync_words(int n_img, int n_pairs, int levels);
-extern "C" int mtb_resident_supported(int w, int h, int levels, int64_t rgb_pitch, int64_t rgb_img_stride);
-int mtb_resident_run(const uint8_t* rgb, int64_t rgb_pitch, int64_t rgb_img_stride, int w, int h, int n_img,
-                     int levels, int tol, const int32_t* pairs_host, int n_pairs, uint32_t* hist_ws,
-                     int32_t* medians, uint64_t* mtb, uint64_t* exclusion, int32_t* acc, unsigned long long* errs,
-                     uint32_t* done, uint32_t* sync_ws, const uint32_t* img_ready, void* stream);
-
 extern "C" int64_t mtb_align_fused_sync_words(int n_img, int n_pairs, int levels) {
-  const int64_t pipe = (int64_t)(n_img + 8) + 2 * (int64_t)n_img + (int64_t)n_pairs * (levels < 1 ? 1 : levels);
-  return std::max(pipe, mtb_resident_sync_words(n_img, n_pairs, levels));
+  return pipe_max_launches(n_img, n_pairs, levels) + 2 * (int64_t)n_img + (int64_t)n_pairs * (levels < 1 ? 1 : levels);
 }
 
 extern "C" int mtb_align_fused_workspace(int w, int h, int levels, int64_t* gray_bytes, int64_t* hist_elems) {
@@ -1409,14 +1289,6 @@ extern "C" int mtb_align_fused_ex(const uint8_t* rgb, int64_t rgb_pitch, int64_t
     MTB_REQUIRE(pairs_host[2 * q] >= 0 && pairs_host[2 * q] < n_img && pairs_host[2 * q + 1] >= 0 &&
                     pairs_host[2 * q + 1] < n_img,
                 "pair image index out of range");
-  }
-  {
-    const char* impl = getenv("MTB_FUSED_IMPL");
-    const bool force_pipe = impl && std::strcmp(impl, "pipe") == 0;
-    if (!force_pipe && mtb_resident_supported(w, h, levels, rgb_pitch, rgb_img_stride) &&
-        (reinterpret_cast<uintptr_t>(rgb) & 7) == 0)
-      return mtb_resident_run(rgb, rgb_pitch, rgb_img_stride, w, h, n_img, levels, tol, pairs_host, n_pairs,
-                              hist_ws, medians, mtb, exclusion, acc, errs, done, sync_ws, img_ready, stream);
   }
   cudaStream_t st = as_stream(stream);
 
@@ -1465,12 +1337,6 @@ extern "C" int mtb_align_fused_ex(const uint8_t* rgb, int64_t rgb_pitch, int64_t
   a.excl = reinterpret_cast<uint32_t*>(exclusion);
   a.bit_img_words32 = 2 * p.bit_img_words;
   a.medians = medians;
-  {
-    const char* pr = getenv("MTB_PIPE_PROBE");
-    a.probe = pr ? atoi(pr) : 0;
-    const char* tr = getenv("MTB_PIPE_TRACE");   // device address of a [J][grid][8] u64 buffer
-    a.trace = tr ? reinterpret_cast<unsigned long long*>(strtoull(tr, nullptr, 0)) : nullptr;
-  }
   a.ctr = sync_ws;
   a.img_ready = img_ready;
   a.acc = acc;
@@ -1487,13 +1353,14 @@ extern "C" int mtb_align_fused_ex(const uint8_t* rgb, int64_t rgb_pitch, int64_t
   a.gray_slots = 3 * B;
   const std::vector<PipeLaunch> plan = pipe_plan(n_img, B, p.n, pairs_host, n_pairs);
   const int J = plan.back().j + 1;
-  // sync_ws (mtb_align_fused_sync_words): [J] K1 tile counters, [n_img]
+  // sync_ws (mtb_align_fused_sync_words): [Jmax] K1 tile counters, [n_img]
   // medians-ready flags, [n_img] K3-done counters, [P][n] decided flags
-  MTB_REQUIRE(J <= n_img + 8, "internal: launch count");
-  const int64_t sync_words = (int64_t)(n_img + 8) + 2 * (int64_t)n_img + (int64_t)n_pairs * p.n;
+  const int64_t jmax = pipe_max_launches(n_img, n_pairs, p.n);
+  MTB_REQUIRE(J <= jmax, "internal: launch count");
+  const int64_t sync_words = jmax + 2 * (int64_t)n_img + (int64_t)n_pairs * p.n;
   MTB_CUDA(cudaMemsetAsync(sync_ws, 0, sizeof(uint32_t) * sync_words, st));
   a.ctr = sync_ws;
-  a.med_ready = sync_ws + n_img + 8;
+  a.med_ready = sync_ws + jmax;
   a.k3_done = a.med_ready + n_img;
   a.decided = a.k3_done + n_img;
   a.n_launch = (int)plan.size();
@@ -1514,11 +1381,8 @@ extern "C" int mtb_align_fused_ex(const uint8_t* rgb, int64_t rgb_pitch, int64_t
       return MTB_ECUDA;
     }
   }
-  static bool attr_done = false;
-  if (!attr_done) {
-    MTB_CUDA(cudaFuncSetAttribute(pipe_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kPipeSmemBytes));
-    attr_done = true;
-  }
+  // the shared-memory opt-in is per device (cheap; set on every call)
+  MTB_CUDA(cudaFuncSetAttribute(pipe_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kPipeSmemBytes));
   const int grid = num_sms() * kPipeCtasPerSm;
   int launches = 0;
   for (const PipeLaunch& L : plan) {
@@ -1530,8 +1394,7 @@ extern "C" int mtb_align_fused_ex(const uint8_t* rgb, int64_t rgb_pitch, int64_t
     a.th_cnt = j >= 1 ? std::max(0, std::min(B, n_img - (j - 1) * B)) : 0;
     a.n_items = 0;
     a.search_tiles = 0;
-    for (const auto& qi : L.items) {
-      MTB_REQUIRE(a.n_items < kPipeMaxItems, "too many pairs in flight for one fused launch");
+    for (const auto& qi : L.items) {   // pipe_plan caps a launch at kPipeMaxItems items
       PipeItem& it = a.items[a.n_items++];
       it.pair = qi.first;
       it.ref = pairs_host[2 * qi.first];
