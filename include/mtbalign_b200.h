@@ -236,6 +236,20 @@ int mtb_search_level_rows(const uint64_t* const* maps, int w, int h, int64_t nwo
                           const int32_t* prev, int64_t prev_stride, const int32_t* base,
                           unsigned long long* errs, int64_t errs_stride, void* stream);
 
+/* mtb_search_level_rows for ONE pair with the target window in up to three
+ * separate buffers (row sharding without concatenating the halos): the
+ * reference maps a_mtb / a_excl hold rows [a_row0, a_row0+a_rows); segment s
+ * (s = 0..2: previous shard's halo, own rows, next shard's halo) holds target
+ * rows [seg_row0[s], seg_row0[s]+seg_rows[s]) in seg[2s] (MTB) / seg[2s+1]
+ * (exclusion), device pointers passed by value (a NULL pair or 0 rows = no
+ * segment).  Rows in no segment, or outside [0, h), contribute 0.  Replaces
+ * the reference's b[y - dy] row reads (kernels/_native.pyx:93-95) for a
+ * shard.  Writes 9 partial counts to errs (zeroed here); no decision. */
+int mtb_search_level_rows3(const uint64_t* a_mtb, const uint64_t* a_excl, int a_row0, int a_rows,
+                           const uint64_t* const* seg, const int* seg_row0, const int* seg_rows, int w, int h,
+                           int64_t nwords64, const int32_t* prev, const int32_t* base, unsigned long long* errs,
+                           void* stream);
+
 /* Threshold + pack every level with GIVEN medians (n_img x n int32): the
  * row-sharded flow all-reduces the histograms first, so every shard
  * thresholds with the medians of the whole image (threshold.py:80-88). */

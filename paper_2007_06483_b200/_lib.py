@@ -55,6 +55,8 @@ SIGNATURES = {
                               _c_void_p],
     "mtb_search_level_rows": [_c_void_p, _i32, _i32, _i64, _i32, _i32, _i32, _i32, _i32, _c_void_p, _i64,
                               _c_void_p, _c_void_p, _i64, _c_void_p],
+    "mtb_search_level_rows3": [_c_void_p, _c_void_p, _i32, _i32, _c_void_p, _c_void_p, _c_void_p, _i32, _i32, _i64,
+                               _c_void_p, _c_void_p, _c_void_p, _c_void_p],
     "mtb_threshold_levels_medians": [_c_void_p, _i32, _i32, _i32, _i32, _i32, _c_void_p, _c_void_p, _c_void_p,
                                      _i32, _c_void_p],
     "mtb_decide_level": [_c_void_p, _i64, _c_void_p, _i64, _c_void_p, _c_void_p, _i64, _i32, _c_void_p],

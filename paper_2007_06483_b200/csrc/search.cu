@@ -129,6 +129,15 @@ struct LevelSearchArgs {
   uint32_t* done;
   int64_t done_stride;
   int tiles_x;                   // ceil(nw32 / 32)
+  // Segmented target (row sharding, SEG kernels): the reference words come
+  // from a_m / a_e (rows [a_row0, a_row0 + a_rows)), the target rows from up
+  // to three buffers, segment s holding image rows [seg_row0[s], +seg_rows[s])
+  // (previous shard's halo, own rows, next shard's halo): no concatenation.
+  const uint32_t* a_m;
+  const uint32_t* a_e;
+  const uint32_t* seg_m[3];
+  const uint32_t* seg_e[3];
+  int seg_row0[3], seg_rows[3];
 };
 
 struct SearchSmem {
@@ -140,6 +149,7 @@ struct SearchSmem {
   int last;
 };
 
+template <bool SEG>
 __global__ void __launch_bounds__(kSTThreads)
 level_search_kernel(LevelSearchArgs a) {
   __shared__ SearchSmem S;
@@ -148,10 +158,10 @@ level_search_kernel(LevelSearchArgs a) {
   const int tx = blockIdx.x % a.tiles_x, ty = blockIdx.x / a.tiles_x;
   const int ly0 = ty * kSTRows, j0 = tx * kSTWords;   // local (reference-window) row of the tile
   const int y0 = a.a_row0 + ly0;                       // image row of the tile
-  const uint32_t* A = reinterpret_cast<const uint32_t*>(a.maps[4 * p + 0]);
-  const uint32_t* EA = reinterpret_cast<const uint32_t*>(a.maps[4 * p + 1]);
-  const uint32_t* B = reinterpret_cast<const uint32_t*>(a.maps[4 * p + 2]);
-  const uint32_t* EB = reinterpret_cast<const uint32_t*>(a.maps[4 * p + 3]);
+  const uint32_t* A = SEG ? a.a_m : reinterpret_cast<const uint32_t*>(a.maps[4 * p + 0]);
+  const uint32_t* EA = SEG ? a.a_e : reinterpret_cast<const uint32_t*>(a.maps[4 * p + 1]);
+  const uint32_t* B = SEG ? nullptr : reinterpret_cast<const uint32_t*>(a.maps[4 * p + 2]);
+  const uint32_t* EB = SEG ? nullptr : reinterpret_cast<const uint32_t*>(a.maps[4 * p + 3]);
 
   int bx = 0, by = 0;
   if (a.prev) {
@@ -183,10 +193,26 @@ level_search_kernel(LevelSearchArgs a) {
     const int i = tid + u * kSTThreads;
     const int r = i / kSTBWords, c = i - r * kSTBWords;
     const int64_t y = (int64_t)sy0 + r, j = sj0 + c;
-    const bool ok = i < kSTBRows * kSTBWords && y >= 0 && y < a.h && y >= a.b_row0 &&
-                    y < a.b_row0 + a.b_rows && j >= 0 && j < a.nw32;
-    rb[u] = ok ? __ldg(B + (y - a.b_row0) * a.nw32 + j) : 0u;
-    reb[u] = ok ? __ldg(EB + (y - a.b_row0) * a.nw32 + j) : 0u;
+    if (SEG) {
+      const uint32_t* pm = nullptr;
+      const uint32_t* pe = nullptr;
+      int64_t ry = 0;
+#pragma unroll
+      for (int sg = 0; sg < 3; ++sg)
+        if (y >= a.seg_row0[sg] && y < (int64_t)a.seg_row0[sg] + a.seg_rows[sg]) {
+          pm = a.seg_m[sg];
+          pe = a.seg_e[sg];
+          ry = y - a.seg_row0[sg];
+        }
+      const bool ok = i < kSTBRows * kSTBWords && pm != nullptr && y >= 0 && y < a.h && j >= 0 && j < a.nw32;
+      rb[u] = ok ? __ldg(pm + ry * a.nw32 + j) : 0u;
+      reb[u] = ok ? __ldg(pe + ry * a.nw32 + j) : 0u;
+    } else {
+      const bool ok = i < kSTBRows * kSTBWords && y >= 0 && y < a.h && y >= a.b_row0 &&
+                      y < a.b_row0 + a.b_rows && j >= 0 && j < a.nw32;
+      rb[u] = ok ? __ldg(B + (y - a.b_row0) * a.nw32 + j) : 0u;
+      reb[u] = ok ? __ldg(EB + (y - a.b_row0) * a.nw32 + j) : 0u;
+    }
   }
 #pragma unroll
   for (int u = 0; u < kAPer; ++u) {
@@ -430,7 +456,7 @@ extern "C" int mtb_find_offset_batch(const uint64_t* const* maps, const int32_t*
     a.decide = 1;
     a.tiles_x = (a.nw32 + kSTWords - 1) / kSTWords;
     const int tiles_y = (a.h + kSTRows - 1) / kSTRows;
-    level_search_kernel<<<dim3(a.tiles_x * tiles_y, P), kSTThreads, 0, st>>>(a);
+    level_search_kernel<false><<<dim3(a.tiles_x * tiles_y, P), kSTThreads, 0, st>>>(a);
     ++launches;
   }
   return check_launch("level_search_kernel", launches);
@@ -466,7 +492,44 @@ extern "C" int mtb_search_level_rows(const uint64_t* const* maps, int w, int h, 
   a.decide = 0;
   a.tiles_x = (a.nw32 + kSTWords - 1) / kSTWords;
   const int tiles_y = (a_rows + kSTRows - 1) / kSTRows;
-  level_search_kernel<<<dim3(a.tiles_x * tiles_y, P), kSTThreads, 0, st>>>(a);
+  level_search_kernel<false><<<dim3(a.tiles_x * tiles_y, P), kSTThreads, 0, st>>>(a);
+  return check_launch("level_search_kernel");
+}
+
+extern "C" int mtb_search_level_rows3(const uint64_t* a_mtb, const uint64_t* a_excl, int a_row0, int a_rows,
+                                      const uint64_t* const* seg, const int* seg_row0, const int* seg_rows, int w,
+                                      int h, int64_t nwords64, const int32_t* prev, const int32_t* base,
+                                      unsigned long long* errs, void* stream) {
+  clear_error();
+  MTB_REQUIRE(a_mtb && a_excl && seg && seg_row0 && seg_rows && errs, "null pointer");
+  MTB_REQUIRE(w >= 1 && h >= 1 && nwords64 * 64 >= w, "bad level dimensions");
+  MTB_REQUIRE(a_rows >= 0 && a_row0 >= 0 && a_row0 + a_rows <= h, "bad row windows");
+  cudaStream_t st = as_stream(stream);
+  MTB_CUDA(cudaMemsetAsync(errs, 0, 9 * sizeof(unsigned long long), st));
+  if (a_rows == 0) return MTB_OK;
+  LevelSearchArgs a{};
+  a.w = w;
+  a.h = h;
+  a.nw32 = (int)(2 * nwords64);
+  a.prev = prev;
+  a.base = base;
+  a.errs = errs;
+  a.a_row0 = a_row0;
+  a.a_rows = a_rows;
+  a.a_m = reinterpret_cast<const uint32_t*>(a_mtb);
+  a.a_e = reinterpret_cast<const uint32_t*>(a_excl);
+  for (int s = 0; s < 3; ++s) {
+    const bool on = seg[2 * s] && seg[2 * s + 1] && seg_rows[s] > 0;
+    MTB_REQUIRE(!on || seg_row0[s] >= -(1 << 30), "bad segment");
+    a.seg_m[s] = on ? reinterpret_cast<const uint32_t*>(seg[2 * s]) : nullptr;
+    a.seg_e[s] = on ? reinterpret_cast<const uint32_t*>(seg[2 * s + 1]) : nullptr;
+    a.seg_row0[s] = on ? seg_row0[s] : 0;
+    a.seg_rows[s] = on ? seg_rows[s] : 0;
+  }
+  a.decide = 0;
+  a.tiles_x = (a.nw32 + kSTWords - 1) / kSTWords;
+  const int tiles_y = (a_rows + kSTRows - 1) / kSTRows;
+  level_search_kernel<true><<<dim3(a.tiles_x * tiles_y, 1), kSTThreads, 0, st>>>(a);
   return check_launch("level_search_kernel");
 }
 

@@ -203,17 +203,15 @@ class MtbEngine:
         """True when the one-launch-per-image pipeline (csrc/pipe.cu) handles this geometry."""
         return self.n <= 6 and (3 * self.width) % 16 == 0
 
-    def fused_workspace(self) -> dict:
-        """Scratch for align_fused: two gray slots (the pipeline keeps them L2-resident)."""
-        t = self.torch
-        ws = getattr(self, "_fused_ws", None)
-        if ws is None:
-            gb = np.zeros(1, dtype=np.int64)
+    def fused_gray_bytes(self) -> int:
+        """Bytes of the fused pipeline's private gray ring (mtb_align_fused_workspace)."""
+        gb = getattr(self, "_fused_gray_bytes", None)
+        if gb is None:
+            arr = np.zeros(1, dtype=np.int64)
             _lib.load().mtb_align_fused_workspace(self.width, self.height, self.requested_levels,
-                                                  gb.ctypes.data_as(_lib._i64p), None)
-            ws = {"gray": t.empty(int(gb[0]), dtype=t.uint8, device="cuda")}
-            self._fused_ws = ws
-        return ws
+                                                  arr.ctypes.data_as(_lib._i64p), None)
+            gb = self._fused_gray_bytes = int(arr[0])
+        return gb
 
     def align_fused(self, rgb, pairs, pyr: PyramidSet | None = None, acc=None, errs=None, done=None,
                     count: bool = True, img_ready=None):
@@ -236,13 +234,14 @@ class MtbEngine:
             errs = t.empty((max(P, 1), self.n, 9), dtype=t.int64, device="cuda")
         if done is None:
             done = t.empty((max(P, 1), self.n), dtype=t.int32, device="cuda")
-        ws = self.fused_workspace()
-        sync = ws.get("sync")
+        # Per-call scratch from torch's stream-aware caching allocator (no
+        # cudaMalloc after the first call): concurrent calls on different
+        # streams never share a gray ring or sync counters.
+        gray = t.empty(self.fused_gray_bytes(), dtype=t.uint8, device="cuda")
         words = int(_lib.load().mtb_align_fused_sync_words(n_img, P, self.n))
-        if sync is None or sync.numel() < words:
-            sync = ws["sync"] = t.empty(words, dtype=t.int32, device="cuda")
+        sync = t.empty(words, dtype=t.int32, device="cuda")
         _lib.call("mtb_align_fused_ex", _dev.ptr(rgb), 3 * self.width, 3 * self.width * self.height, self.width,
-                  self.height, n_img, self.requested_levels, self.tol, pairs.ctypes.data, P, _dev.ptr(ws["gray"]),
+                  self.height, n_img, self.requested_levels, self.tol, pairs.ctypes.data, P, _dev.ptr(gray),
                   _dev.ptr(pyr.hist_ws), _dev.ptr(pyr.medians), _dev.ptr(pyr.mtb), _dev.ptr(pyr.excl),
                   _dev.ptr(acc), _dev.ptr(errs), _dev.ptr(done), _dev.ptr(sync),
                   _dev.ptr(img_ready) if img_ready is not None else None, _dev.stream())
@@ -272,16 +271,11 @@ class MtbEngine:
                 self.height, self.width, 3):
             raise ValueError(f"host batch must be a CPU uint8 (N, {self.height}, {self.width}, 3) tensor")
         n_img = int(host.shape[0])
-        ws = self.fused_workspace()
         if dev is None:
             dev = t.empty(tuple(host.shape), dtype=t.uint8, device="cuda")
-        ready = ws.get("ready")
-        if ready is None or ready.numel() < n_img:
-            ready = ws["ready"] = t.empty(max(n_img, 8), dtype=t.int32, device="cuda")
-        cs = ws.get("copy_stream")
-        if cs is None:
-            cs = ws["copy_stream"] = t.cuda.Stream()
         cur = t.cuda.current_stream()
+        ready = t.empty(max(n_img, 8), dtype=t.int32, device="cuda")   # per call (see align_fused)
+        cs = t.cuda.Stream()
         cs.wait_stream(cur)            # dev / ready no longer in use by earlier work
         with t.cuda.stream(cs):
             ready[:n_img].zero_()
@@ -293,6 +287,7 @@ class MtbEngine:
                 dev[i].copy_(host[i], non_blocking=True)
             _lib.call("mtb_stream_write_u32", _dev.ptr(ready[i]), 1, cs.cuda_stream)
         dev.record_stream(cs)
+        ready.record_stream(cs)
         pyr, acc, errs = self.align_fused(dev, pairs, pyr, acc, errs, done, count=count, img_ready=ready)
         cur.wait_stream(cs)
         return dev, pyr, acc, errs

@@ -72,9 +72,16 @@ def to_grayscale(img):
     return _dev.like_input(out, img)
 
 
-def _offsets_tensor(offsets):
+def _clamp_offset(dx: int, dy: int, w: int, h: int):
+    """Any integer offset, clamped to [-(w+1), w+1] x [-(h+1), h+1]: beyond the
+    raster every pixel is fill either way (image.py:82-106 accepts any int), and
+    the clamp keeps the values inside the kernels' int32 arithmetic."""
+    return max(-(w + 1), min(w + 1, int(dx))), max(-(h + 1), min(h + 1, int(dy)))
+
+
+def _offsets_tensor(offsets, w: int, h: int):
     torch = _dev.torch_mod()
-    arr = np.asarray([[int(o[0]), int(o[1])] for o in offsets], dtype=np.int32)
+    arr = np.asarray([_clamp_offset(o[0], o[1], w, h) for o in offsets], dtype=np.int32).reshape(-1, 2)
     return torch.from_numpy(arr).to("cuda")
 
 
@@ -86,7 +93,7 @@ def shift_rgb_device(batch, offsets, fill=(0, 0, 0), out=None):
     torch = _dev.torch_mod()
     n, h, w = int(batch.shape[0]), int(batch.shape[1]), int(batch.shape[2])
     if not _dev.is_tensor(offsets):
-        offsets = _offsets_tensor(offsets)
+        offsets = _offsets_tensor(offsets, w, h)
     offsets = offsets.to(torch.int32).contiguous()
     if out is None:
         out = torch.empty_like(batch)
@@ -112,6 +119,6 @@ def shift_gray(img, offset: ShiftOffset, fill: int = 0):
     src = _dev.to_device(img)
     h, w = int(src.shape[0]), int(src.shape[1])
     out = torch.empty_like(src)
-    _lib.call("mtb_shift_gray", _dev.ptr(src), w, w, h, int(offset[0]), int(offset[1]), int(fill) & 0xFF,
-              _dev.ptr(out), w, _dev.stream())
+    dx, dy = _clamp_offset(offset[0], offset[1], w, h)
+    _lib.call("mtb_shift_gray", _dev.ptr(src), w, w, h, dx, dy, int(fill) & 0xFF, _dev.ptr(out), w, _dev.stream())
     return _dev.like_input(out, img)

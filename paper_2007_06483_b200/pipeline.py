@@ -3,19 +3,30 @@
 `align_stack` keeps the reference's contract: chain alignment (image i+1
 against image i), offsets re-based onto image 0 by prefix sums, image 0
 passed through untouched, per-stage timings that tile the call.  The work
-behind it is batched on the device: every image's MTB pyramid is built by
-one fused preprocess over the whole stack, all N-1 searches run as one
-batched coarse-to-fine search, and all outputs are shifted in one launch.
+behind it is batched on the device: every image's MTB pyramid and every
+pair's coarse-to-fine search run in one batched pass, the cumulative offsets
+are summed on the device and all outputs are shifted in one launch.
 
-Stage windows (host wall clock, synchronised at each boundary):
+Path selection (`use_fused`): images of >= 4 MP go through the fused
+pipeline (csrc/pipe.cu: preprocess and search of the whole stack in one
+pipelined launch sequence, 15 % faster at 24 MP); smaller ones through the
+staged kernels (one persistent K1 launch over the whole batch wins there:
+config 1 352 K vs 43 K pairs/s).
+
+Stage windows (pipeline.py:74-112) are CUDA events recorded on the stream at
+the stage boundaries, read after ONE synchronisation at the end of the call
+(no device-wide syncs inside it); host time after the last event is added
+to the last stage, so the stages still sum to the call's wall time:
   grayscale  host -> device upload of the stack
-  pyramid    fused gray + pyramid + per-level histograms (one RGB pass)
-  threshold  medians + MTB / exclusion packing of every level
-  search     batched find_offset + readback of offsets and traces
-  shift      batched shift_rgb + download of the aligned images
+  pyramid    fused gray + pyramid + histograms (staged), or the whole fused
+             pipeline (preprocess, thresholds and search overlap there)
+  threshold  medians + MTB / exclusion packing (staged; 0 in fused mode)
+  search     batched find_offset (staged) + readback of offsets and traces
+  shift      device prefix sums, batched shift_rgb, download of the outputs
 
 Additions over the reference API (north star): `align` (chain or pivot
-pairing — config 3 aligns a 7-exposure stack to its middle exposure) and
+pairing — config 3 aligns a 7-exposure stack to its middle exposure),
+`align_stacks` (many same-size stacks in one device batch) and
 `get_exp_shift` (one pair; OpenCV/Ward naming of find_offset on RGB input).
 """
 
@@ -110,61 +121,142 @@ def upload_stack(images):
     return host.to("cuda", non_blocking=True)
 
 
-def _sync():
-    _dev.torch_mod().cuda.synchronize()
+FUSED_MIN_PIXELS = 4_000_000   # fused pipeline at >= 4 MP, staged kernels below
 
 
-def _align(images, pairs, levels, tol, layout, pivot):
-    """Shared body of align_stack / align: pairs are (ref, tgt) image indices."""
+def use_fused(eng: MtbEngine) -> bool:
+    """True when the fused pipeline is the faster path for this engine's images."""
+    return eng.fused_supported and eng.width * eng.height >= FUSED_MIN_PIXELS
+
+
+class _StageClock:
+    """CUDA events at stage boundaries on the current stream; one sync at the end."""
+
+    def __init__(self):
+        self.torch = _dev.torch_mod()
+        self.t0 = time.perf_counter()
+        self.events = []
+        self.mark()
+
+    def mark(self):
+        ev = self.torch.cuda.Event(enable_timing=True)
+        ev.record()
+        self.events.append(ev)
+
+    def timings(self, names):
+        """Stage durations in ms (events[i] -> events[i+1]); host time after
+        the last event (result unpacking) is charged to the last stage."""
+        self.events[-1].synchronize()
+        wall = (time.perf_counter() - self.t0) * 1000.0
+        out = {n: self.events[i].elapsed_time(self.events[i + 1]) for i, n in enumerate(names)}
+        rest = max(0.0, wall - sum(out.values()))
+        out[names[-1]] += rest
+        return out
+
+
+def _pairs_for(n: int, mode: str, pivot):
+    if mode == "chain":
+        return [(i, i + 1) for i in range(n - 1)], None
+    if mode != "pivot":
+        raise ValueError(f"mode must be 'chain' or 'pivot', got {mode!r}")
+    p = n // 2 if pivot is None else int(pivot)
+    if not 0 <= p < n:
+        raise ValueError(f"pivot {p} out of range for {n} images")
+    return [(p, i) for i in range(n) if i != p], p
+
+
+def _run_batch(eng: MtbEngine, batch, pairs, clk: _StageClock):
+    """Preprocess + search of a device batch; marks pyramid / threshold / search."""
+    n_img = int(batch.shape[0])
+    if use_fused(eng):
+        _, acc, errs = eng.align_fused(batch, pairs)
+        clk.mark()          # pyramid: the whole pipelined sequence
+        clk.mark()          # threshold: inside it
+    else:
+        pyr = eng.alloc(n_img)
+        eng.pyramid_hist(batch, pyr)
+        clk.mark()
+        eng.threshold_levels(pyr, n_img)
+        counters.bump(PYRAMID_BUILDS, n_img)
+        counters.bump(MTB_PYRAMID_BUILDS, n_img)
+        clk.mark()
+        acc, errs = eng.search(pyr, pairs)
+    return acc, errs
+
+
+def _device_cumulative(acc, n_img: int, pairs, anchor):
+    """(n_img, 2) int32 device offsets onto the anchor: prefix sums of the
+    chain's pairwise offsets (pipeline.py:91-93), or each pair's own offset
+    against the pivot."""
+    torch = _dev.torch_mod()
+    cum = torch.zeros((n_img, 2), dtype=torch.int32, device="cuda")
+    if anchor is None:
+        cum[1:] = torch.cumsum(acc[:, 0], dim=0, dtype=torch.int32)
+    else:
+        tgts = torch.tensor([t for _, t in pairs], dtype=torch.long, device="cuda")
+        cum.index_copy_(0, tgts, acc[:, 0].to(torch.int32))
+    return cum
+
+
+def _align_batch(images, stacks, levels, tol, layout, mode, pivot):
+    """Shared body of align_stack / align / align_stacks.  `stacks` = list of
+    (first image index, count) of the same-size stacks inside `images`."""
     w, h = _validate_stack(images)
     _check_layout(layout)
-    n_img = len(images)
-    timings = {}
-    t0 = time.perf_counter()
+    torch = _dev.torch_mod()
+    clk = _StageClock()
     eng = engine_for(w, h, levels, tol)
     batch = upload_stack(images)
-    _sync()
-    t1 = time.perf_counter()
-    pyr = eng.alloc(n_img)
-    eng.pyramid_hist(batch, pyr)
-    _sync()
-    t2 = time.perf_counter()
-    eng.threshold_levels(pyr, n_img)
-    counters.bump(PYRAMID_BUILDS, n_img)
-    counters.bump(MTB_PYRAMID_BUILDS, n_img)
-    _sync()
-    t3 = time.perf_counter()
-    acc, errs = eng.search(pyr, pairs)
-    pairwise = results_from_device(acc, errs)
-    # Re-basing: chain mode sums the pairwise offsets (pipeline.py:91-93); in
-    # pivot mode every pair already measures image i against the pivot.
-    cumulative = [ShiftOffset(0, 0)] * n_img
-    if pivot is None:
-        for i, res in enumerate(pairwise, start=1):
-            cumulative[i] = cumulative[i - 1] + res.offset
-    else:
-        for (ref, tgt), res in zip(pairs, pairwise):
-            cumulative[tgt] = res.offset
-    t4 = time.perf_counter()
-    anchor = 0 if pivot is None else pivot
-    movers = [i for i in range(n_img) if i != anchor]
-    torch = _dev.torch_mod()
+    clk.mark()
+    pairs, anchors = [], []
+    for i0, n in stacks:
+        ps, anchor = _pairs_for(n, mode, pivot)
+        pairs += [(i0 + r, i0 + t) for r, t in ps]
+        anchors.append(anchor)
+    acc, errs = _run_batch(eng, batch, pairs, clk)
+    acc_h = torch.empty(tuple(acc.shape), dtype=acc.dtype, pin_memory=True)
+    errs_h = torch.empty(tuple(errs.shape), dtype=errs.dtype, pin_memory=True)
+    acc_h.copy_(acc, non_blocking=True)
+    errs_h.copy_(errs, non_blocking=True)
+    clk.mark()
+    # shift: every non-anchor image onto its stack's anchor, offsets stay on the device
+    cum, movers = [], []
+    q = 0
+    for (i0, n), anchor in zip(stacks, anchors):
+        np_ = n - 1
+        cum.append(_device_cumulative(acc[q:q + np_], n, [(r - i0, t - i0) for r, t in pairs[q:q + np_]], anchor))
+        keep = 0 if anchor is None else anchor
+        movers += [i0 + i for i in range(n) if i != keep]
+        q += np_
+    cum = torch.cat(cum)
     idx = torch.tensor(movers, dtype=torch.long, device="cuda")
-    shifted = shift_rgb_device(batch.index_select(0, idx).contiguous(), [cumulative[i] for i in movers])
-    aligned = list(images)
+    shifted = shift_rgb_device(batch.index_select(0, idx).contiguous(), cum.index_select(0, idx).contiguous())
     as_numpy = isinstance(images[0], np.ndarray)
-    host = shifted.cpu().numpy() if as_numpy else shifted
+    if as_numpy:
+        host = torch.empty(tuple(shifted.shape), dtype=torch.uint8, pin_memory=True)
+        host.copy_(shifted, non_blocking=True)
+    clk.mark()
+    timings = clk.timings(STAGES)
+    out_imgs = list(images)
+    src = host.numpy() if as_numpy else shifted
     for j, i in enumerate(movers):
-        aligned[i] = host[j]
-    _sync()
-    t5 = time.perf_counter()
-    timings["grayscale"] = (t1 - t0) * 1000.0
-    timings["pyramid"] = (t2 - t1) * 1000.0
-    timings["threshold"] = (t3 - t2) * 1000.0
-    timings["search"] = (t4 - t3) * 1000.0
-    timings["shift"] = (t5 - t4) * 1000.0
-    record = StackAlignment(image_count=n_img, pairwise=pairwise, cumulative=cumulative, timings=timings)
-    return aligned, record
+        out_imgs[i] = src[j]
+    results = []
+    q = 0
+    for (i0, n), anchor in zip(stacks, anchors):
+        np_ = n - 1
+        pairwise = results_from_device(acc_h[q:q + np_], errs_h[q:q + np_])
+        cumulative = [ShiftOffset(0, 0)] * n
+        if anchor is None:
+            for i, res in enumerate(pairwise, start=1):
+                cumulative[i] = cumulative[i - 1] + res.offset
+        else:
+            for (_, tgt), res in zip(pairs[q:q + np_], pairwise):
+                cumulative[tgt - i0] = res.offset
+        record = StackAlignment(image_count=n, pairwise=pairwise, cumulative=cumulative, timings=dict(timings))
+        results.append((out_imgs[i0:i0 + n], record))
+        q += np_
+    return results
 
 
 def align_stack(images: list, levels: int = DEFAULT_LEVELS, tol: int = DEFAULT_NOISE_TOLERANCE,
@@ -175,8 +267,8 @@ def align_stack(images: list, levels: int = DEFAULT_LEVELS, tol: int = DEFAULT_N
     object.  `workers` is accepted for API compatibility; the device batches
     every image and pair regardless, so results never depend on it.
     """
-    n = len(images)
-    return _align(images, [(i, i + 1) for i in range(n - 1)], levels, tol, layout, None)
+    (aligned, record), = _align_batch(list(images), [(0, len(images))], levels, tol, layout, "chain", None)
+    return aligned, record
 
 
 def align(images: list, levels: int = DEFAULT_LEVELS, tol: int = DEFAULT_NOISE_TOLERANCE,
@@ -189,16 +281,35 @@ def align(images: list, levels: int = DEFAULT_LEVELS, tol: int = DEFAULT_NOISE_T
     untouched.  Each pair is find_offset(mtb[pivot], mtb[i]).
     """
     n = len(images)
-    if mode == "chain":
-        return align_stack(images, levels, tol, layout)
-    if mode != "pivot":
+    if mode not in ("chain", "pivot"):
         raise ValueError(f"mode must be 'chain' or 'pivot', got {mode!r}")
     if n < 2:
         raise ValueError(f"alignment needs at least 2 images; got {n}")
-    p = n // 2 if pivot is None else int(pivot)
-    if not 0 <= p < n:
-        raise ValueError(f"pivot {p} out of range for {n} images")
-    return _align(images, [(p, i) for i in range(n) if i != p], levels, tol, layout, p)
+    _pairs_for(n, mode, pivot)   # validates the pivot
+    (aligned, record), = _align_batch(list(images), [(0, n)], levels, tol, layout, mode, pivot)
+    return aligned, record
+
+
+def align_stacks(stacks: list, levels: int = DEFAULT_LEVELS, tol: int = DEFAULT_NOISE_TOLERANCE,
+                 layout: str = PACKED, mode: str = "chain", pivot: int | None = None):
+    """Align many same-size stacks in ONE device batch: every
+    stack's pyramids and searches run in one pass, every output in one shift
+    launch.  Returns [(aligned images, StackAlignment)] in input order; each
+    record carries the batch's stage timings.  Results equal per-stack
+    `align(stack, mode=mode, pivot=pivot)` calls."""
+    stacks = [list(st) for st in stacks]
+    if not stacks:
+        return []
+    if mode not in ("chain", "pivot"):
+        raise ValueError(f"mode must be 'chain' or 'pivot', got {mode!r}")
+    images, spans = [], []
+    for st in stacks:
+        if len(st) < 2:
+            raise ValueError(f"alignment needs at least 2 images; got {len(st)}")
+        _pairs_for(len(st), mode, pivot)
+        spans.append((len(images), len(st)))
+        images += st
+    return _align_batch(images, spans, levels, tol, layout, mode, pivot)
 
 
 def get_exp_shift(ref_rgb, tgt_rgb, levels: int = DEFAULT_LEVELS, tol: int = DEFAULT_NOISE_TOLERANCE) -> ShiftOffset:
@@ -206,7 +317,7 @@ def get_exp_shift(ref_rgb, tgt_rgb, levels: int = DEFAULT_LEVELS, tol: int = DEF
     w, h = _validate_stack([ref_rgb, tgt_rgb])
     eng = engine_for(w, h, levels, tol)
     batch = upload_stack([ref_rgb, tgt_rgb])
-    if eng.fused_supported:
+    if use_fused(eng):
         _, acc, _ = eng.align_fused(batch, [(0, 1)])     # one pipelined launch sequence (csrc/pipe.cu)
     else:
         pyr = eng.preprocess(batch)
@@ -233,15 +344,7 @@ def align_files(paths, levels: int = DEFAULT_LEVELS, tol: int = DEFAULT_NOISE_TO
     n = len(paths)
     if n < 2:
         raise ValueError(f"alignment needs at least 2 images; got {n}")
-    if mode == "chain":
-        pairs, anchor = [(i, i + 1) for i in range(n - 1)], None
-    elif mode == "pivot":
-        anchor = n // 2 if pivot is None else int(pivot)
-        if not 0 <= anchor < n:
-            raise ValueError(f"pivot {anchor} out of range for {n} images")
-        pairs = [(anchor, i) for i in range(n) if i != anchor]
-    else:
-        raise ValueError(f"mode must be 'chain' or 'pivot', got {mode!r}")
+    pairs, anchor = _pairs_for(n, mode, pivot)
     t0 = time.perf_counter()
     host = load_stack(paths, workers=workers, pinned=True)
     t1 = time.perf_counter()
@@ -249,7 +352,7 @@ def align_files(paths, levels: int = DEFAULT_LEVELS, tol: int = DEFAULT_NOISE_TO
     if w < MIN_LEVEL_SIZE or h < MIN_LEVEL_SIZE:
         raise ValueError(f"images must be at least 16x16; got {w}x{h}")
     eng = engine_for(w, h, levels, tol)
-    if eng.fused_supported:
+    if use_fused(eng):
         batch, _, acc, errs = eng.align_fused_host(host, pairs)
     else:
         batch = host.to("cuda", non_blocking=True)

@@ -9,23 +9,30 @@ The only configuration whose data path has a real exchange step:
   * each shard builds gray + pyramid + per-level histograms of its rows
     (K1), then the 2 x n x 256 histograms are SUM-all-reduced so every shard
     thresholds with the medians of the whole image (threshold.py:80-88);
+  * the shifted target rows a shard needs beyond its own come from its two
+    neighbours only: at level k the base dy is 2 * acc(k+1) with
+    |acc(j)| <= 2^(n-j) - 1, so the candidates read at most 2^(n-k) - 1 rows
+    past either edge (`halo_rows`).  Shards hold >= 2 blocks of 2^(n-1) rows,
+    so that halo is always shorter than a neighbour's rows.  These worst-case
+    halos of every level are exchanged ONCE per pair, right after the
+    threshold pass, in one batched neighbour send/recv (NCCL P2P over
+    NVLink); nothing depends on the chosen offsets on the host;
   * per level (deepest first) each shard counts the 9 candidate errors over
-    its own reference rows; the shifted target rows it needs beyond its own
-    (|by|+1 rows, by = the level's base dy) come from the neighbouring shards
-    (halo exchange); the 9 counts are SUM-all-reduced and every shard applies
-    the same search.py:67 key, so all shards agree on the offset.
+    its own reference rows against [previous halo | own rows | next halo]
+    (three buffers, mtb_search_level_rows3: no concatenation), the 9 counts
+    are SUM-all-reduced and every shard applies the same search.py:67 key on
+    the device, so all shards agree on the offset without a host round trip.
 
-Collectives per pair: 1 histogram all-reduce + n x (halo all-gather + one
-9-count all-reduce).  `Comm` wraps torch.distributed (NCCL on GPUs, gloo in
-the CPU tests); `align_pair_loopback` drives W virtual shards in one process
-(same phase functions, sums done in place) for single-GPU verification.
+Collectives per pair: 1 histogram all-reduce + 1 batched halo exchange + n
+9-count all-reduces; the level loop has no host synchronisation.
+`align_pair_loopback` drives W virtual shards in one process (same phase
+functions, sums done in place) for single-GPU verification.
 """
 
 from __future__ import annotations
 
-from dataclasses import dataclass
+import ctypes
 
-import numpy as np
 
 from . import _dev, _lib
 from .image import ShiftOffset
@@ -36,11 +43,12 @@ from .search import NEIGHBORHOOD, AlignmentResult, LevelTrace
 # ------------------------------------------------------------------ geometry --
 def plan_row_shards(height: int, n_levels: int, world: int) -> list[tuple[int, int]]:
     """[r0, r1) level-0 row range per shard; r0 multiples of 2^(n-1), the
-    remainder rows (< 2^(n-1)) go to the last shard."""
+    remainder rows (< 2^(n-1)) go to the last shard.  Every shard gets >= 2
+    blocks so its neighbours' worst-case halos (`halo_rows`) fit in it."""
     block = 1 << (n_levels - 1)
     blocks = height // block
-    if blocks < world:
-        raise ValueError(f"{height} rows make {blocks} blocks of {block}; fewer than {world} shards")
+    if blocks < 2 * world:
+        raise ValueError(f"{height} rows make {blocks} blocks of {block}; need >= 2 per shard for {world} shards")
     out, b0 = [], 0
     for r in range(world):
         nb = blocks // world + (1 if r < blocks % world else 0)
@@ -54,6 +62,12 @@ def plan_row_shards(height: int, n_levels: int, world: int) -> list[tuple[int, i
 
 def level_rows(r0: int, r1: int, k: int) -> tuple[int, int]:
     return r0 >> k, r1 >> k
+
+
+def halo_rows(n_levels: int, k: int) -> int:
+    """Worst-case target rows needed past either shard edge at level k:
+    |base dy| + 1 <= 2 (2^(n-1-k) - 1) + 1 = 2^(n-k) - 1 (search.py:85-95)."""
+    return (1 << (n_levels - k)) - 1
 
 
 def halo_sizes(by: int) -> tuple[int, int]:
@@ -107,36 +121,36 @@ class CudaShard:
         return (self.mtb[img, off:off + h_loc * nw].view(h_loc, nw),
                 self.excl[img, off:off + h_loc * nw].view(h_loc, nw))
 
-    def slabs(self, k: int, hp: int, hn: int):
-        """Top hn rows and bottom hp rows of the target maps (both maps stacked)."""
+    def edges(self, k: int, rows: int):
+        """((mtb, excl) of the first `rows`, (mtb, excl) of the last `rows`) target
+        rows of level k: contiguous views, sent to the neighbours as halos."""
         m, e = self.level_maps(k, 1)
-        top = self.torch.stack([m[:hn], e[:hn]])
-        bot = self.torch.stack([m[m.shape[0] - hp:], e[e.shape[0] - hp:]])
-        return top.contiguous(), bot.contiguous()
+        return (m[:rows], e[:rows]), (m[m.shape[0] - rows:], e[e.shape[0] - rows:])
 
-    def count_level(self, k: int, lead, tail, prev_dev):
-        """9 partial error counts of level k over this shard's reference rows.
+    def halo_buffers(self, k: int, rows: int):
+        nw = int(self.geom[k, 4])
+        t = self.torch
+        return (t.empty((rows, nw), dtype=t.int64, device="cuda"), t.empty((rows, nw), dtype=t.int64, device="cuda"))
 
-        lead: the previous shard's last target rows (2 maps stacked) or None;
-        tail: the next shard's first target rows, or None (the halo)."""
+    def count_level(self, k: int, lead, tail, prev_dev, halo: int):
+        """9 partial error counts (1, 9) of level k over this shard's reference rows
+        against the target window [lead | own | tail]; lead / tail = (mtb, excl)
+        halo buffers of `halo` rows from the neighbours, or None at an image edge."""
         t = self.torch
         am, ae = self.level_maps(k, 0)
         bm, be = self.level_maps(k, 1)
-        parts_m = [x for x in (lead[0] if lead is not None else None, bm, tail[0] if tail is not None else None)
-                   if x is not None]
-        parts_e = [x for x in (lead[1] if lead is not None else None, be, tail[1] if tail is not None else None)
-                   if x is not None]
-        ext_m, ext_e = t.cat(parts_m).contiguous(), t.cat(parts_e).contiguous()
         y0, y1 = level_rows(self.r0, self.r1, k)
-        b_row0 = y0 - (lead.shape[1] if lead is not None else 0)
         w_k, nw = int(self.geom[k, 0]), int(self.geom[k, 4])
-        table = t.tensor([[am.data_ptr(), ae.data_ptr(), ext_m.data_ptr(), ext_e.data_ptr()]], dtype=t.int64,
-                         device="cuda")
+        segs = (ctypes.c_void_p * 6)(
+            lead[0].data_ptr() if lead is not None else None, lead[1].data_ptr() if lead is not None else None,
+            bm.data_ptr(), be.data_ptr(),
+            tail[0].data_ptr() if tail is not None else None, tail[1].data_ptr() if tail is not None else None)
+        row0 = (ctypes.c_int * 3)(y0 - halo, y0, y1)
+        rows = (ctypes.c_int * 3)(halo if lead is not None else 0, y1 - y0, halo if tail is not None else 0)
         errs = t.empty((1, 9), dtype=t.int64, device="cuda")
-        _lib.call("mtb_search_level_rows", _dev.ptr(table), w_k, self.H >> k, nw, y0, y1 - y0, b_row0,
-                  int(ext_m.shape[0]), 1, _dev.ptr(prev_dev) if prev_dev is not None else None, 2,
-                  None, _dev.ptr(errs), 9, _dev.stream())
-        self._keep = (ext_m, ext_e, table)  # alive until the stream has consumed them
+        _lib.call("mtb_search_level_rows3", am.data_ptr(), ae.data_ptr(), y0, y1 - y0, segs, row0, rows, w_k,
+                  self.H >> k, nw, _dev.ptr(prev_dev) if prev_dev is not None else None, None, _dev.ptr(errs),
+                  _dev.stream())
         return errs
 
     def decide(self, errs_sum, prev_dev):
@@ -175,8 +189,8 @@ def align_pair_loopback(ref_rgb, tgt_rgb, world: int, levels: int = 10, tol: int
                         shard_cls=CudaShard) -> AlignmentResult:
     """Row-sharded find_offset of one pair with `world` virtual shards in ONE
     process: the same per-shard phases as the NCCL path, the collectives
-    replaced by in-process sums / slab hand-offs.  Bit-identical to the
-    unsharded path (tests/test_gpu_sharded.py)."""
+    replaced by in-process sums and halo hand-offs (neighbour edge views).
+    Bit-identical to the unsharded path (tests/test_gpu_sharded.py)."""
     H, W = int(ref_rgb.shape[0]), int(ref_rgb.shape[1])
     n = pair_levels(W, H, levels)
     rows = plan_row_shards(H, n, world)
@@ -185,24 +199,55 @@ def align_pair_loopback(ref_rgb, tgt_rgb, world: int, levels: int = 10, tol: int
     ghist = sum(hists[1:], hists[0])
     for sh in shards:
         sh.threshold(ghist)
+    accs, errs_all = loopback_levels(shards, n)
+    return _result([a[0].tolist() for a in accs], [e[0].tolist() for e in errs_all], n)
+
+
+def loopback_levels(shards, n: int):
+    """The coarse-to-fine level loop over in-process shards; returns the
+    per-level device tensors (chosen offset (1, 2), summed counts (1, 9)).
+    Issues no synchronising call (tests/test_gpu_sharded.py)."""
+    world = len(shards)
     prev, accs, errs_all = None, [None] * n, [None] * n
     for k in reversed(range(n)):
-        by = 0 if prev is None else 2 * int(prev[0, 1])
-        hp, hn = halo_sizes(by)
-        sl = [sh.slabs(k, hp, hn) for sh in shards]
-        parts = []
-        for r, sh in enumerate(shards):
-            lead = sl[r - 1][1] if r > 0 and hp > 0 else None
-            tail = sl[r + 1][0] if r + 1 < world and hn > 0 else None
-            parts.append(sh.count_level(k, lead, tail, prev))
-        total = sum(parts[1:], parts[0])
-        acc = shards[0].decide(total, prev)
-        accs[k], errs_all[k] = np.asarray(acc[0].tolist()), np.asarray(total[0].tolist())
-        prev = acc
-    return _result(accs, errs_all, n)
+        hk = halo_rows(n, k)
+        edges = [sh.edges(k, hk) for sh in shards]
+        parts = [sh.count_level(k, edges[r - 1][1] if r > 0 else None, edges[r + 1][0] if r + 1 < world else None,
+                                prev, hk) for r, sh in enumerate(shards)]
+        total = parts[0]
+        for p in parts[1:]:
+            total = total + p
+        prev = shards[0].decide(total, prev)
+        accs[k], errs_all[k] = prev, total
+    return accs, errs_all
 
 
 # ------------------------------------------------------------- NCCL driver --
+def exchange_halos(shard, n: int, rank: int, world: int):
+    """Every level's worst-case halos in ONE batched neighbour exchange:
+    this shard's first rows go to rank-1 (its `tail`), its last rows to rank+1
+    (its `lead`).  Returns {k: (lead, tail)} (None at the image edges)."""
+    import torch.distributed as dist
+
+    ops, out = [], {}
+    for k in range(n):
+        hk = halo_rows(n, k)
+        top, bot = shard.edges(k, hk)
+        lead = shard.halo_buffers(k, hk) if rank > 0 else None
+        tail = shard.halo_buffers(k, hk) if rank + 1 < world else None
+        if lead is not None:
+            ops += [dist.P2POp(dist.isend, top[0], rank - 1), dist.P2POp(dist.isend, top[1], rank - 1),
+                    dist.P2POp(dist.irecv, lead[0], rank - 1), dist.P2POp(dist.irecv, lead[1], rank - 1)]
+        if tail is not None:
+            ops += [dist.P2POp(dist.isend, bot[0], rank + 1), dist.P2POp(dist.isend, bot[1], rank + 1),
+                    dist.P2POp(dist.irecv, tail[0], rank + 1), dist.P2POp(dist.irecv, tail[1], rank + 1)]
+        out[k] = (lead, tail)
+    if ops:
+        for req in dist.batch_isend_irecv(ops):
+            req.wait()
+    return out
+
+
 def align_pair_distributed(ref_rows, tgt_rows, width: int, height: int, levels: int = 10, tol: int = 4,
                            shard_cls=CudaShard) -> AlignmentResult:
     """SPMD: call on every rank of an initialised torch.distributed group with
@@ -218,20 +263,12 @@ def align_pair_distributed(ref_rows, tgt_rows, width: int, height: int, levels: 
     hist = shard.preprocess(shard.stack_rows(ref_rows, tgt_rows))
     dist.all_reduce(hist, op=dist.ReduceOp.SUM)                   # 2 x n x 256 histograms
     shard.threshold(hist)
+    halos = exchange_halos(shard, n, rank, world)                 # all levels, one batched P2P
     prev, accs, errs_all = None, [None] * n, [None] * n
-    for k in reversed(range(n)):
-        by = 0 if prev is None else 2 * int(prev[0, 1])
-        hp, hn = halo_sizes(by)
-        top, bot = shard.slabs(k, hp, hn)
-        tops = [top.new_empty(top.shape) for _ in range(world)]
-        bots = [bot.new_empty(bot.shape) for _ in range(world)]
-        dist.all_gather(tops, top)                                 # halo exchange
-        dist.all_gather(bots, bot)
-        lead = bots[rank - 1] if rank > 0 and hp > 0 else None
-        tail = tops[rank + 1] if rank + 1 < world and hn > 0 else None
-        errs = shard.count_level(k, lead, tail, prev)
+    for k in reversed(range(n)):                                  # no host synchronisation in here
+        lead, tail = halos[k]
+        errs = shard.count_level(k, lead, tail, prev, halo_rows(n, k))
         dist.all_reduce(errs, op=dist.ReduceOp.SUM)               # 9 counts
-        acc = shard.decide(errs, prev)
-        accs[k], errs_all[k] = np.asarray(acc[0].tolist()), np.asarray(errs[0].tolist())
-        prev = acc
-    return _result(accs, errs_all, n)
+        prev = shard.decide(errs, prev)
+        accs[k], errs_all[k] = prev, errs
+    return _result([a[0].tolist() for a in accs], [e[0].tolist() for e in errs_all], n)

@@ -1,6 +1,6 @@
 """CPU stand-in for CudaShard (test infrastructure): the same per-shard
 phases computed with the numpy oracle, so the row-sharded orchestration
-(histogram all-reduce, halo all-gather, 9-count all-reduce) can be exercised
+(histogram all-reduce, neighbour halo exchange, 9-count all-reduce) can be exercised
 with gloo on CPU."""
 
 import numpy as np
@@ -40,13 +40,16 @@ class OracleShard:
                 self.maps[i][k] = (orc.mtb_mask(g, med).astype(np.uint8),
                                    orc.exclusion_mask(g, med, self.tol).astype(np.uint8))
 
-    def slabs(self, k, hp, hn):
+    def edges(self, k, rows):
         m, e = self.maps[1][k]
-        top = torch.from_numpy(np.stack([m[:hn], e[:hn]]).copy())
-        bot = torch.from_numpy(np.stack([m[m.shape[0] - hp:], e[e.shape[0] - hp:]]).copy())
-        return top, bot
+        return ((torch.from_numpy(m[:rows].copy()), torch.from_numpy(e[:rows].copy())),
+                (torch.from_numpy(m[m.shape[0] - rows:].copy()), torch.from_numpy(e[e.shape[0] - rows:].copy())))
 
-    def count_level(self, k, lead, tail, prev):
+    def halo_buffers(self, k, rows):
+        w = self.maps[1][k][0].shape[1]
+        return torch.empty((rows, w), dtype=torch.uint8), torch.empty((rows, w), dtype=torch.uint8)
+
+    def count_level(self, k, lead, tail, prev, halo):
         am, ae = self.maps[0][k]
         bm, be = self.maps[1][k]
         parts_m = [p for p in (lead[0].numpy() if lead is not None else None, bm,
@@ -55,7 +58,7 @@ class OracleShard:
                                tail[1].numpy() if tail is not None else None) if p is not None]
         ext_m, ext_e = np.concatenate(parts_m), np.concatenate(parts_e)
         y0, y1 = level_rows(self.r0, self.r1, k)
-        b0 = y0 - (lead.shape[1] if lead is not None else 0)
+        b0 = y0 - (halo if lead is not None else 0)
         hk, wk = self.H >> k, am.shape[1]
         bx, by = (0, 0) if prev is None else (2 * int(prev[0, 0]), 2 * int(prev[0, 1]))
         errs = np.zeros(9, np.int64)
