@@ -45,9 +45,12 @@ def parse():
     ap.add_argument("--steps", type=int, default=200)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", choices=("ours", "reference"), default="ours")
-    ap.add_argument("--pairs", type=int, default=32, help="pairs per step per GPU")
-    ap.add_argument("--width", type=int, default=6000)
-    ap.add_argument("--height", type=int, default=4000)
+    ap.add_argument("--config", type=int, choices=(1, 2, 3, 4), default=2,
+                    help="BASELINE.json config: 1 = 1024x768 pairs, 2 = 24 MP pairs (default, the headline), "
+                         "3 = 7 x 24 MP stacks aligned to the middle exposure, 4 = 12 MP pairs")
+    ap.add_argument("--pairs", type=int, default=0, help="pairs (config 3: stacks) per step per GPU; 0 = config default")
+    ap.add_argument("--width", type=int, default=0)
+    ap.add_argument("--height", type=int, default=0)
     ap.add_argument("--levels", type=int, default=6)
     ap.add_argument("--tol", type=int, default=4)
     ap.add_argument("--mode", choices=("fused", "staged"), default="fused",
@@ -60,7 +63,37 @@ def parse():
     ap.add_argument("--cpu-reps", type=int, default=3)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
-    return ap.parse_args()
+    ap.add_argument("--no-oracle-check", action="store_true", help="skip checking every benched pair on the CPU")
+    args = ap.parse_args()
+    dflt = CONFIGS[args.config]
+    args.width = args.width or dflt["width"]
+    args.height = args.height or dflt["height"]
+    args.pairs = args.pairs or dflt["units"]
+    args.stack = dflt["stack"]
+    if args.config == 1 and "--mode" not in " ".join(sys.argv):
+        args.mode = "staged"   # small images: one persistent K1 launch over the batch wins
+    return args
+
+
+# BASELINE.json configs as bench workloads: `units` per step per GPU of
+# `stack` images each (pairs: stack 2; config 3: 7-exposure stacks aligned to
+# their middle exposure, 6 pairs each).  Config 5 (one gigapixel pair,
+# row-sharded) is measured by tools/config5.py, not here.
+CONFIGS = {
+    1: {"width": 1024, "height": 768, "units": 512, "stack": 2},
+    2: {"width": 6000, "height": 4000, "units": 32, "stack": 2},
+    3: {"width": 6000, "height": 4000, "units": 8, "stack": 7},
+    4: {"width": 4000, "height": 3000, "units": 64, "stack": 2},
+}
+
+
+def unit_pairs(n_units: int, stack: int):
+    """(ref, tgt) image pairs of n_units stacks of `stack` images: pairs for
+    stack 2, else every exposure against the stack's middle one."""
+    if stack == 2:
+        return [(2 * u, 2 * u + 1) for u in range(n_units)]
+    mid = stack // 2
+    return [(stack * u + mid, stack * u + i) for u in range(n_units) for i in range(stack) if i != mid]
 
 
 def load_peak():
@@ -135,21 +168,35 @@ class ClockSampler:
 
 
 # ------------------------------------------------------- CPU reference --
-def reference_images(width, height, seed=1):
-    """The bounded CPU sample: one exposure pair from the device generator's recipe
-    (same base/shift/tone construction), built with numpy here."""
+def reference_images(width, height, stack=2, seed=1):
+    """The bounded CPU sample: one exposure pair (or one 7-exposure config-3
+    stack) from the device generator's recipe, built with numpy here."""
     sys.path.insert(0, os.path.join(ROOT, "oracle"))
     import mtb_oracle as orc
 
     rng = np.random.default_rng(seed)
     base = np.dstack([orc.synthetic_gray(rng, width, height) for _ in range(3)])
-    imgs, man = orc.generate_stack(base, 2, seed=seed, max_shift=63)
-    return imgs, man
+    if stack == 2:
+        return orc.generate_stack(base, 2, seed=seed, max_shift=63)
+    return orc.generate_stack(base, stack, seed=seed, max_shift=20, gains=[2 ** ((k - 3) / 3) for k in range(stack)],
+                              gammas=[1.0] * stack)
 
 
-def time_reference(width, height, levels, tol, reps):
-    """Reference align_stack (oracle/_ref, compiled engine) on all host cores; pairs/s."""
-    imgs, man = reference_images(width, height)
+def cpu_model():
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return None
+
+
+def time_reference(width, height, levels, tol, reps, stack=2):
+    """Reference align_stack (oracle/_ref, compiled engine) on all host cores and
+    on one worker; pairs/s (a stack of k images is k-1 chained pairs)."""
+    imgs, man = reference_images(width, height, stack)
     cores = os.cpu_count() or 1
     kind = "reference"
     try:
@@ -158,47 +205,67 @@ def time_reference(width, height, levels, tol, reps):
 
         assert ref.kernels.engine_name() == "native"
 
-        def run():
-            _, rec = ref.align_stack(imgs, levels=levels, tol=tol, workers=cores)
-            return tuple(rec.cumulative[1])
+        def run(workers):
+            _, rec = ref.align_stack(imgs, levels=levels, tol=tol, workers=workers)
+            return tuple(rec.cumulative[-1])
     except Exception:
         import mtb_oracle as orc
 
         kind, cores = "port", 1
 
-        def run():
+        def run(workers):
             _, _, cum = orc.align_stack(imgs, levels, tol)
-            return tuple(cum[1])
-    got = run()  # warm-up
-    times = []
-    for _ in range(max(1, reps)):
-        t0 = time.perf_counter()
-        run()
-        times.append(time.perf_counter() - t0)
-    best = min(times)
-    return {"value": 1.0 / best, "unit": UNIT, "cores": cores, "kind": kind,
-            "sample": f"1 pair {width}x{height} RGB8, {levels} levels, align_stack(workers={cores}), best of "
-                      f"{len(times)} after 1 warm-up; ms/pair {best * 1e3:.1f}; offset {got}"}
+            return tuple(cum[-1])
+
+    def best_of(workers):
+        got = run(workers)  # warm-up
+        times = []
+        for _ in range(max(1, reps)):
+            t0 = time.perf_counter()
+            run(workers)
+            times.append(time.perf_counter() - t0)
+        return min(times), got, len(times)
+
+    best, got, n = best_of(cores)
+    best1, _, _ = best_of(1) if cores > 1 else (best, None, n)
+    pairs = stack - 1
+    what = "1 pair" if stack == 2 else f"1 {stack}-exposure stack ({pairs} chained pairs)"
+    return {"value": pairs / best, "unit": UNIT, "cores": cores, "kind": kind,
+            "sample": f"{what} {width}x{height} RGB8, {levels} levels, align_stack(workers={cores}), best of "
+                      f"{n} after 1 warm-up; ms {best * 1e3:.1f}; last cumulative offset {got}",
+            "workers_1": {"value": pairs / best1, "unit": UNIT, "ms": round(best1 * 1e3, 1)},
+            "cpu_model": cpu_model()}
 
 
 # ------------------------------------------------------------- our arm --
-def make_inputs(torch, eng, pairs, seed):
-    """(2*pairs, H, W, 3) device batch: pair p = (exposure a, shifted+toned exposure b)."""
+def make_inputs(torch, eng, units, stack, seed):
+    """(units*stack, H, W, 3) device batch of synthetic exposure stacks (the
+    SURVEY 8(d) recipe: synth.py generate_stack on a synthetic base; config 3
+    uses the gains 2^((k-3)/3), gamma 1, max shift 20).  Returns the batch and
+    each pair's ground-truth offset (target onto reference)."""
     from paper_2007_06483_b200.image import shift_rgb_device
     from paper_2007_06483_b200.synth import apply_lut_device, draw_manifest, synthetic_rgb_device, tone_lut
 
     h, w = eng.height, eng.width
-    batch = torch.empty((2 * pairs, h, w, 3), dtype=torch.uint8, device="cuda")
+    batch = torch.empty((stack * units, h, w, 3), dtype=torch.uint8, device="cuda")
     truth = []
-    n_bases = min(pairs, 4)
+    n_bases = min(units, 4)
     bases = [synthetic_rgb_device(seed + b, w, h) for b in range(n_bases)]
-    for p in range(pairs):
-        pw, cum, gains, gammas = draw_manifest(2, seed=seed + p, max_shift=63)
-        base = bases[p % n_bases]
-        apply_lut_device(base, tone_lut(gains[0], gammas[0]), out=batch[2 * p])
-        moved = shift_rgb_device(base.unsqueeze(0), [(-cum[1].dx, -cum[1].dy)])[0]
-        apply_lut_device(moved, tone_lut(gains[1], gammas[1]), out=batch[2 * p + 1])
-        truth.append((cum[1].dx, cum[1].dy))
+    for u in range(units):
+        if stack == 2:
+            pw, cum, gains, gammas = draw_manifest(2, seed=seed + u, max_shift=63)
+        else:
+            pw, cum, gains, gammas = draw_manifest(stack, seed=seed + u, max_shift=20,
+                                                   gains=[2 ** ((k - 3) / 3) for k in range(stack)],
+                                                   gammas=[1.0] * stack)
+        base = bases[u % n_bases]
+        for i in range(stack):
+            moved = shift_rgb_device(base.unsqueeze(0), [(-cum[i].dx, -cum[i].dy)])[0]
+            apply_lut_device(moved, tone_lut(gains[i], gammas[i]), out=batch[stack * u + i])
+        mid = stack // 2 if stack > 2 else 0
+        for i in range(stack):
+            if i != mid:
+                truth.append((cum[i].dx - cum[mid].dx, cum[i].dy - cum[mid].dy))
     torch.cuda.synchronize()
     return batch, truth
 
@@ -214,11 +281,11 @@ def run_ours(args, rank, world, local_rank):
         import torch.distributed as dist
 
     eng = mtb.MtbEngine(args.width, args.height, args.levels, args.tol)
-    P = args.pairs
-    n_img = 2 * P
-    batch, truth = make_inputs(torch, eng, P, seed=1000 * rank + 1)
+    n_img = args.pairs * args.stack
+    pairs = unit_pairs(args.pairs, args.stack)
+    P = len(pairs)
+    batch, truth = make_inputs(torch, eng, args.pairs, args.stack, seed=1000 * rank + 1)
     pyr = eng.alloc(n_img)
-    pairs = [(2 * p, 2 * p + 1) for p in range(P)]
     table = eng.maps_table(pyr, pairs)
     acc = torch.empty((P, eng.n, 2), dtype=torch.int32, device="cuda")
     errs = torch.empty((P, eng.n, 9), dtype=torch.int64, device="cuda")
@@ -338,23 +405,33 @@ def run_ours(args, rank, world, local_rank):
         k1_avg_s /= n_launch_fused
         k1_bytes /= n_launch_fused
     achieved = k1_bytes / k1_avg_s / 1e9
+    if fused:
+        # pipe_kernel is 100 % of a fused step (ncu launch list, profiles/): its
+        # achieved rate is the timed graph replays' algorithmic bytes / time
+        achieved = n_img * img_bytes / (elapsed / args.steps) / 1e9
     traffic = load_traffic("pipe_kernel" if fused else "k1_rgb_pyramid_kernel")
-    step_gbs = value / world * 2 * img_bytes / 1e9
+    step_gbs = value / world * (n_img * img_bytes / P) / 1e9   # algorithmic bytes per pair = the step's RGB / pairs
 
+    # every benched pair re-checked on the CPU (reference engine when built)
+    oracle = None if args.no_oracle_check else oracle_check(args, torch, batch, pairs, acc, errs)
     e2e = None
     if not args.no_e2e:
-        e2e = run_e2e(args, torch, eng, batch, pyr, table, acc, errs, done, P)
+        e2e = run_e2e(args, torch, eng, batch, pyr, table, acc, errs, done, pairs)
     with_out = None
-    if fused and not args.no_e2e:
+    if fused and not args.no_e2e and args.stack == 2:
         with_out = run_with_output(args, torch, eng, batch, pyr, acc, errs, done, P)
+    latency = single_pair_latency(torch, mtb, batch) if args.config == 2 and not args.no_e2e else None
 
     out = {
         "metric": METRIC, "value": round(value, 2), "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": max(3, args.warmup), "ms_per_step": round(elapsed / args.steps * 1e3, 4),
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u8", "data": "synthetic",
-        "config": {"workload": f"{P} x {args.width * args.height / 1e6:.0f}MP ({args.width}x{args.height}) RGB8 exposure pairs per GPU per step, "
-                               f"{args.levels} levels, tol {args.tol} (BASELINE config "
-                               f"{ {(6000, 4000): 2, (1024, 768): 1, (4000, 3000): 4, (40000, 25000): 5}.get((args.width, args.height), 'custom')}, batched)",
+        "config": {"workload": (f"{P} x {args.width * args.height / 1e6:.0f}MP ({args.width}x{args.height}) RGB8 exposure pairs per GPU per step, "
+                                if args.stack == 2 else
+                                f"{args.pairs} x {args.stack}-exposure {args.width * args.height / 1e6:.0f}MP ({args.width}x{args.height}) RGB8 stacks "
+                                f"aligned to their middle exposure ({P} pairs) per GPU per step, ")
+                               + f"{args.levels} levels, tol {args.tol} (BASELINE config {args.config}, batched)",
+                   "baseline_config": args.config,
                    "width": args.width, "height": args.height, "levels": args.levels, "tol": args.tol,
                    "pairs_per_step_per_gpu": P, "preprocess_chunk_images": chunk, "k1_images_per_launch": k1_images,
                    "discard_gray": not args.keep_gray,
@@ -363,10 +440,11 @@ def run_ours(args, rank, world, local_rank):
                    "launch": "cuda-graph replay per step" if graph is not None else "python launches",
                    "mode": args.mode,
                    "correct_offsets": f"{correct}/{P} match ground truth"},
+        "oracle_match": oracle,
         "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
                      "frac": round(achieved / peak, 4), "traffic": traffic, "peak_source": peak_src,
                      "kernel": (f"pipe_kernel (fused K1+K3+K4, {_lib.load().mtb_align_fused_images_per_launch(args.width, args.height)} image(s) per launch, "
-                                f"{n_launch_fused} PDL launches per step)") if fused else
+                                f"{n_launch_fused} PDL launches per step = 100% of the step; achieved = step RGB bytes / timed step)") if fused else
                                f"k1_rgb_pyramid_kernel (K1: RGB->gray->pyramid->histograms, {k1_images} images/launch)",
                      "algorithmic_bytes_per_launch": k1_bytes, "avg_launch_ms": round(k1_avg_s * 1e3, 4),
                      "whole_step_gbs": round(step_gbs, 1), "whole_step_frac": round(step_gbs / peak, 4)},
@@ -377,7 +455,90 @@ def run_ours(args, rank, world, local_rank):
         out["e2e"] = e2e
     if with_out is not None:
         out["with_output"] = with_out
+    if latency is not None:
+        out["single_pair_latency"] = latency
     return out
+
+
+def oracle_check(args, torch, batch, pairs, acc, errs):
+    """Copy every benched pair back and run it through the reference's own
+    engine (oracle/_ref, mtbalign 0.1.0 + its Cython kernels) on all host
+    cores: offset and all 9 x n error counts must match.  Falls back to the
+    numpy restatement (oracle/mtb_oracle.py) when the reference is not built.
+    Exits non-zero on any mismatch."""
+    import concurrent.futures as cf
+
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    t0 = time.perf_counter()
+    try:
+        sys.path.insert(0, os.path.join(ROOT, "oracle", "_ref"))
+        import mtbalign as ref
+
+        kind = "reference (oracle/_ref, native engine)"
+
+        def pyr_of(img):
+            return ref.build_mtb_pyramid(ref.build_pyramid(ref.to_grayscale(img), args.levels), args.tol)
+
+        def search(a, b):
+            r = ref.find_offset(a, b)
+            return tuple(r.offset), {t.level: [e for _, e in t.candidates] for t in r.traces}
+    except Exception:
+        import mtb_oracle as orc
+
+        kind = "port (oracle/mtb_oracle.py)"
+
+        def pyr_of(img):
+            return orc.preprocess(img, args.levels, args.tol)["mtb"]
+
+        def search(a, b):
+            r = orc.find_offset(a, b)
+            return tuple(r["offset"]), {t["level"]: [e for _, e in t["candidates"]] for t in r["traces"]}
+
+    acc_h, errs_h = acc.cpu().numpy(), errs.cpu().numpy()
+    imgs_needed = sorted({i for p in pairs for i in p})
+    workers = os.cpu_count() or 1
+    pyrs = {}
+    with cf.ThreadPoolExecutor(max_workers=workers) as pool:
+        futs = {}
+        for i in imgs_needed:   # one image on the host at a time per worker slot
+            futs[i] = pool.submit(pyr_of, batch[i].cpu().numpy())
+            if len(futs) >= 2 * workers:
+                for j, f in list(futs.items()):
+                    pyrs[j] = f.result()
+                futs = {}
+        for j, f in futs.items():
+            pyrs[j] = f.result()
+        results = list(pool.map(lambda pq: search(pyrs[pq[0]], pyrs[pq[1]]), pairs))
+    bad = []
+    for q, (off, tr) in enumerate(results):
+        ok = tuple(acc_h[q, 0].tolist()) == off and all(errs_h[q, k].tolist() == tr[k] for k in tr)
+        if not ok:
+            bad.append(q)
+    line = {"matched": f"{len(pairs) - len(bad)}/{len(pairs)}", "checker": kind,
+            "what": "offset + all 9 x levels candidate error counts of every benched pair",
+            "seconds": round(time.perf_counter() - t0, 1)}
+    if bad:
+        print(json.dumps({"oracle_mismatch": bad[:16], **line}), file=sys.stderr, flush=True)
+        raise SystemExit(f"oracle mismatch on pairs {bad[:16]}")
+    return line
+
+
+def single_pair_latency(torch, mtb, batch):
+    """Paper-style one-pair alignment (config 2): get_exp_shift on one
+    device-resident 24 MP pair, CUDA events, median of 10 after 3 warm-ups."""
+    a, b = batch[0], batch[1]
+    for _ in range(3):
+        mtb.get_exp_shift(a, b)
+    times = []
+    for _ in range(10):
+        s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        s.record()
+        mtb.get_exp_shift(a, b)
+        e.record()
+        e.synchronize()
+        times.append(s.elapsed_time(e))
+    return {"ms_median": round(statistics.median(times), 4), "ms_best": round(min(times), 4),
+            "api": "get_exp_shift (fused pipeline, device-resident pair, includes the offset readback)"}
 
 
 def _world_max_time(dt):
@@ -425,15 +586,15 @@ def run_with_output(args, torch, eng, batch, pyr, acc, errs, done, P):
             "bytes_per_pair": 12 * w * h, "note": "align_fused + shift_rgb of each target (device offsets), python launches"}
 
 
-def run_e2e(args, torch, eng, batch, pyr, table, acc, errs, done, P):
+def run_e2e(args, torch, eng, batch, pyr, table, acc, errs, done, pairs):
     """Same metric through the public engine API from pinned HOST buffers: every step
     copies the step's RGB pairs H2D and reads the offsets back D2H (timed)."""
+    P = len(pairs)
     host = torch.empty(batch.shape, dtype=torch.uint8, pin_memory=True)
     host.copy_(batch)
     out_host = torch.empty((P, 2), dtype=torch.int32, pin_memory=True)
     dev_in = torch.empty_like(batch)
     stream = torch.cuda.current_stream()
-    n_img = 2 * P
 
     fused = args.mode == "fused"
 
@@ -447,7 +608,6 @@ def run_e2e(args, torch, eng, batch, pyr, table, acc, errs, done, P):
             eng.search_table(table_in, P, acc, errs, done, count=False)
         out_host.copy_(acc[:, 0], non_blocking=True)
 
-    pairs = [(2 * p, 2 * p + 1) for p in range(P)]
     table_in = eng.maps_table(pyr, pairs)
     for _ in range(2):
         step()
@@ -466,8 +626,25 @@ def run_e2e(args, torch, eng, batch, pyr, table, acc, errs, done, P):
                     if args.mode == "fused" else "MtbEngine.preprocess + search_table on an H2D-copied pinned batch")}
 
 
+def spawn_ranks(n: int) -> int:
+    """`bench.py --gpus N` outside torchrun: re-launch this command under
+    torch.distributed.run with N ranks (one per GPU, 127.0.0.1 rendezvous);
+    rank 0 prints the line."""
+    import socket
+    import subprocess
+
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr=127.0.0.1", f"--master-port={port}", os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.call(cmd)
+
+
 def main():
     args = parse()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ and args.impl == "ours":
+        raise SystemExit(spawn_ranks(args.gpus))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
@@ -475,13 +652,15 @@ def main():
     if args.impl == "reference":
         if rank != 0:
             return
-        cb = time_reference(args.width, args.height, args.levels, args.tol, args.cpu_reps)
+        cb = time_reference(args.width, args.height, args.levels, args.tol, args.cpu_reps, args.stack)
         line = {"metric": METRIC, "value": round(cb["value"], 4), "unit": UNIT, "n_gpus": args.gpus,
                 "steps": args.cpu_reps, "warmup": 1, "ms_per_step": round(1e3 / cb["value"], 2),
                 "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u8",
                 "data": "synthetic", "impl": "reference",
-                "config": {"workload": f"1 x {args.width * args.height / 1e6:.0f}MP ({args.width}x{args.height}) RGB8 pair per step, "
-                                       f"{args.levels} levels, tol {args.tol}"},
+                "config": {"workload": (f"1 x {args.width * args.height / 1e6:.0f}MP ({args.width}x{args.height}) RGB8 pair per step, "
+                                        if args.stack == 2 else
+                                        f"1 x {args.stack}-exposure {args.width * args.height / 1e6:.0f}MP stack per step, ")
+                                       + f"{args.levels} levels, tol {args.tol} (BASELINE config {args.config})"},
                 "cpu_baseline": cb,
                 "e2e": {"value": round(cb["value"], 4), "unit": UNIT, "h2d_bytes_per_step": 0,
                         "d2h_bytes_per_step": 0}}
@@ -493,6 +672,8 @@ def main():
     if world > 1:
         import torch.distributed as dist
 
+        if torch.cuda.device_count() < world:
+            raise SystemExit(f"--gpus {world} needs {world} visible GPUs; {torch.cuda.device_count()} present")
         torch.cuda.set_device(local_rank)
         dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
     else:
@@ -500,7 +681,8 @@ def main():
     out = run_ours(args, rank, world, local_rank)
     if rank == 0:
         if world == 1 and not args.no_cpu_baseline:
-            out["cpu_baseline"] = time_reference(args.width, args.height, args.levels, args.tol, args.cpu_reps)
+            out["cpu_baseline"] = time_reference(args.width, args.height, args.levels, args.tol, args.cpu_reps,
+                                                 args.stack)
         print(json.dumps(out), flush=True)
     if world > 1:
         import torch.distributed as dist

@@ -163,7 +163,8 @@ def test_fused_plan_more_pairs_than_one_launch(mtb, cuda, n_img):
     from paper_2007_06483_b200.synth import generate_stack, synthetic_rgb_device
 
     w, h = 256, 192
-    imgs, _ = generate_stack(synthetic_rgb_device(3, w, h), n_img, seed=3, max_shift=6)
+    steps = [(1 + (i % 3), 1) if i % 2 == 0 else (-(1 + (i % 3)), -1) for i in range(n_img - 1)]   # bounded drift
+    imgs, _ = generate_stack(synthetic_rgb_device(3, w, h), n_img, pairwise=steps, seed=3)
     batch = cuda.stack(imgs).contiguous()
     pairs = [(n_img - 1, i) for i in range(n_img - 1)]
     eng = mtb.MtbEngine(w, h, 6, 4)
