@@ -149,6 +149,16 @@ __device__ __forceinline__ void grid_dep_launch() { asm volatile("griddepcontrol
 // CTAs are all resident once its successor runs (a launch can only start
 // after every CTA of its predecessor has started), so spinning cannot
 // deadlock.
+// CTA-scope flag handoffs in shared memory (release store / acquire load).
+__device__ __forceinline__ int ld_acquire_cta(const int* p) {
+  int v;
+  asm volatile("ld.acquire.cta.shared::cta.u32 %0, [%1];" : "=r"(v) : "r"(smem_addr(p)) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release_cta(int* p, int v) {
+  asm volatile("st.release.cta.shared::cta.u32 [%0], %1;" ::"r"(smem_addr(p)), "r"(v) : "memory");
+}
+
 __device__ __forceinline__ uint32_t ld_relaxed(const uint32_t* p) {
   uint32_t v;
   asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
@@ -844,8 +854,7 @@ __device__ __forceinline__ int aux_phase_of(const PipeArgs& a, int q) {
 // warp to reach such a task waits for them and fills S.th; others wait on
 // S.th_state.  Search tasks (first in the queue) run meanwhile.
 __device__ __forceinline__ void aux_need_thresholds(const PipeArgs& a, PipeSmem& S, int lane) {
-  volatile int* st = &S.th_state;
-  if (*st == 2) return;
+  if (ld_acquire_cta(&S.th_state) == 2) return;
   int claim = 0;
   if (lane == 0) claim = atomicCAS(&S.th_state, 0, 1) == 0;
   claim = __shfl_sync(0xffffffffu, claim, 0);
@@ -862,13 +871,12 @@ __device__ __forceinline__ void aux_need_thresholds(const PipeArgs& a, PipeSmem&
       c.med_lo = med <= 127;
       S.th[b][k] = c;
     }
-    __threadfence_block();
     __syncwarp();
-    if (lane == 0) *st = 2;
+    if (lane == 0) st_release_cta(&S.th_state, 2);
   } else {
-    while (*st != 2) __nanosleep(32);
+    while (ld_acquire_cta(&S.th_state) != 2) __nanosleep(32);
   }
-  __threadfence_block();
+  __syncwarp();
 }
 
 __device__ __forceinline__ void aux_drain(const PipeArgs& a, PipeSmem& S, const AuxCtx& x) {
@@ -1144,18 +1152,14 @@ __global__ void __launch_bounds__(kPipeThreads, kPipeCtasPerSm) pipe_kernel(cons
     }
     // Join the aux work (the aux prologue has long finished: spin on its flag).
     if constexpr (kPAuxWarps > 0) {
-      while (*reinterpret_cast<volatile int*>(&S.aux_ready) == 0) __nanosleep(64);
-      __threadfence_block();
+      while (ld_acquire_cta(&S.aux_ready) == 0) __nanosleep(64);
     } else {
       aux_prologue(a, S, tid, kPipeThreads, 9);
     }
   } else {
     // ======================= aux warps: K3 + search ==========================
     aux_prologue(a, S, tid - 32 * kPK1Warps, 32 * kPAuxWarps, 6);
-    if (tid == 32 * kPK1Warps) {
-      __threadfence_block();
-      *reinterpret_cast<volatile int*>(&S.aux_ready) = 1;
-    }
+    if (tid == 32 * kPK1Warps) st_release_cta(&S.aux_ready, 1);
   }
 
   // ============ every warp: this CTA's share of the aux tasks ================
