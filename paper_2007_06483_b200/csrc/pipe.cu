@@ -164,11 +164,20 @@ __device__ __forceinline__ uint32_t ld_relaxed(const uint32_t* p) {
   asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
   return v;
 }
-// Poll with relaxed loads and acquire once the value is reached: an acquire
-// load at gpu scope invalidates the SM's L1 (CCTL.IVALL) on every poll.
-// MTB_SPIN_LIMIT (debug builds) bounds the spin: a lost flag then fails the
-// launch (trap) instead of hanging the GPU.
+__device__ __forceinline__ uint32_t ld_acquire(const uint32_t* p) {
+  uint32_t v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+// Wait until *p >= v with acquire semantics.  Usually the flag is already
+// set: one acquire load.  Otherwise poll with relaxed loads (an acquire load
+// at gpu scope invalidates the SM's L1, CCTL.IVALL, so polling with it would
+// do that on every iteration) and acquire once with a final acquire load
+// (cheaper than a gpu-scope fence, which waits for all the warp's
+// outstanding memory operations).  MTB_SPIN_LIMIT (debug builds) bounds the
+// spin: a lost flag then fails the launch (trap) instead of hanging the GPU.
 __device__ __forceinline__ void spin_geq(const uint32_t* p, uint32_t v) {
+  if (ld_acquire(p) >= v) return;
 #ifdef MTB_SPIN_LIMIT
   long long n = 0;
   while (ld_relaxed(p) < v) {
@@ -178,7 +187,7 @@ __device__ __forceinline__ void spin_geq(const uint32_t* p, uint32_t v) {
 #else
   while (ld_relaxed(p) < v) __nanosleep(100);
 #endif
-  asm volatile("fence.acq_rel.gpu;" ::: "memory");
+  (void)ld_acquire(p);
 }
 
 // Lower median of one level's spread histogram (threshold.py:31-39): the

@@ -1,5 +1,13 @@
-# A/B: current build vs exp/$1.so, alternating
-for i in 1 2; do
-for lib in paper_2007_06483_b200/_lib/libmtbalign_b200.so paper_2007_06483_b200/_lib/exp/$1.so; do
- echo "$(basename $lib): $(MTB_LIB_PATH=$PWD/$lib timeout 120 python bench.py --mode fused --steps 40 --no-cpu-baseline --no-e2e 2>/dev/null | python -c 'import json,sys; d=json.loads(sys.stdin.read()); print(d["value"], d["ms_per_step"])')"
-done; done
+#!/usr/bin/env bash
+# Same-box A/B: current library vs _lib/exp/$1.so, alternating bench runs.  Usage: tools/ab.sh NAME [bench args]
+cd "$(dirname "$0")/.."
+name=$1; shift
+L=$PWD/paper_2007_06483_b200/_lib/exp/$name.so
+for i in 1 2 3; do
+  for v in cur $name; do
+    if [ $v = cur ]; then unset MTB_LIB_PATH; else export MTB_LIB_PATH=$L; fi
+    r=$(timeout 300 python bench.py --steps 60 --warmup 5 --no-e2e --no-cpu-baseline --no-oracle-check "$@" 2>/dev/null | grep -o '"value": [0-9.]*' | head -1)
+    echo "$v $r"
+  done
+done
+unset MTB_LIB_PATH
