@@ -43,6 +43,7 @@ namespace mtb {
 
 constexpr int kPipeMaxLevels = 6;
 constexpr int kPipeMaxItems = 96;
+constexpr int kPipeImgs = 2;                  // images per launch (K1 part and K3 part)
 constexpr int kPipeThreads = 512;     // 12 K1 warps + 4 aux warps
 constexpr int kPipeCtasPerSm = 1;
 constexpr int kPipeWarps = kPipeThreads / 32;
@@ -84,6 +85,8 @@ struct PipeArgs {
   int j;                             // this launch's index
   int k1_img0, k1_cnt;               // images k1_img0 .. +k1_cnt-1 of the K1 part (k1_cnt may be 0)
   int gray_slots;                    // gray ring slots in use: 3 x images per launch
+  uint8_t* k1_gray[kPipeImgs];       // ring slot of each K1 image of this launch (host-computed: no
+  const uint8_t* th_gray[kPipeImgs]; //   integer modulo per tile / task), and of each K3 image
   int th_img0, th_cnt;               // images of the K3 part
   int n_items;
   int search_tiles;
@@ -105,7 +108,6 @@ constexpr int kPK1Groups = 3;
 constexpr int kPK1Warps = 4 * kPK1Groups;
 constexpr int kPAuxWarps = kPipeWarps - kPK1Warps;
 constexpr int kPStages = 2;
-constexpr int kPipeImgs = 2;                  // images per launch (K1 part and K3 part)
 constexpr int kPGraySlots = 3 * kPipeImgs;    // gray ring capacity: written, being read, lagging readers
                                               // (3 x images per launch slots in use)
 constexpr int kAuxPhases = 7;     // aux task phases: K3 levels 0..3, levels 4..5, padding, search
@@ -782,9 +784,7 @@ __device__ __forceinline__ int aux_phase_tasks1(const PipeArgs& a, int p) {
 __device__ __forceinline__ int aux_phase_tasks(const PipeArgs& a, int p) {
   return p < 6 ? a.th_cnt * aux_phase_tasks1(a, p) : a.search_tiles;
 }
-__device__ __forceinline__ const uint8_t* aux_slot(const PipeArgs& a, int b) {
-  return a.g.gray + (int64_t)((a.th_img0 + b) % a.gray_slots) * a.g.gray_img_stride;
-}
+__device__ __forceinline__ const uint8_t* aux_slot(const PipeArgs& a, int b) { return a.th_gray[b]; }
 __device__ __forceinline__ uint32_t* aux_mtb(const PipeArgs& a, int b) {
   return a.mtb + (int64_t)(a.th_img0 + b) * a.bit_img_words32;
 }
@@ -1104,7 +1104,7 @@ __global__ void __launch_bounds__(kPipeThreads, kPipeCtasPerSm) pipe_kernel(cons
         if (k > 0 && a.g.nl >= 5 && wg == ((k - 1) & 3))
           k1_levels45_tm(a.g, ptg, S.l3[g][(k - 1) & 1], ptx, pty, lane, phb, pfull);
         const int img = a.k1_img0 + b;
-        uint8_t* tg = a.g.gray + (int64_t)(img % a.gray_slots) * a.g.gray_img_stride + (int64_t)tile * kTileGrayBytes;
+        uint8_t* tg = a.k1_gray[b] + (int64_t)tile * kTileGrayBytes;
         const uint32_t hbi = hb + (uint32_t)b * (6 * 256 * 4);
         uint8_t* l3_slot = &S.l3[g][k & 1][wg][lane];
         if (full)
@@ -1405,6 +1405,10 @@ extern "C" int mtb_align_fused_ex(const uint8_t* rgb, int64_t rgb_pitch, int64_t
     a.k1_cnt = std::max(0, std::min(B, n_img - j * B));
     a.th_img0 = (j - 1) * B;
     a.th_cnt = j >= 1 ? std::max(0, std::min(B, n_img - (j - 1) * B)) : 0;
+    for (int b = 0; b < kPipeImgs; ++b) {
+      a.k1_gray[b] = gray_ws + (int64_t)((a.k1_img0 + b) % a.gray_slots) * g.gray_img_stride;
+      a.th_gray[b] = gray_ws + (int64_t)(((a.th_img0 + b) % a.gray_slots + a.gray_slots) % a.gray_slots) * g.gray_img_stride;
+    }
     a.n_items = 0;
     a.search_tiles = 0;
     for (const auto& qi : L.items) {   // pipe_plan caps a launch at kPipeMaxItems items
