@@ -13,7 +13,7 @@ sys.path.insert(0, ROOT)
 import paper_2007_06483_b200 as mtb  # noqa: E402
 from paper_2007_06483_b200.synth import generate_stack, synthetic_rgb_device  # noqa: E402
 
-w, h = 512, 384
+w, h = (int(sys.argv[1]), int(sys.argv[2])) if len(sys.argv) > 2 else (512, 384)
 imgs, _ = generate_stack(synthetic_rgb_device(1, w, h), 8, seed=1, max_shift=12)
 batch = torch.stack(imgs).contiguous()
 pairs = [(i, i + 1) for i in range(7)] + [(0, 7)]
