@@ -307,3 +307,36 @@ def test_acceptance_6_mtb_exposure_invariance(mtb, cuda):
         before = mtb.make_mtb_pair(img).mtb.to_bool()
         after = mtb.make_mtb_pair(curve[img]).mtb.to_bool()
         assert np.array_equal(before, after)
+
+
+def test_concurrent_fused_calls_on_two_streams(mtb, cuda):
+    """Two host threads run align_fused on the SAME engine on different
+    streams at once: per-call scratch (gray ring, sync words) keeps them
+    independent; results equal the serial ones."""
+    import threading
+
+    from paper_2007_06483_b200.synth import generate_stack, synthetic_rgb_device
+
+    w, h = 2048, 1536
+    eng = mtb.MtbEngine(w, h, 6, 4)
+    batches = [cuda.stack(generate_stack(synthetic_rgb_device(30 + i, w, h), 6, seed=30 + i, max_shift=20)[0])
+               for i in range(2)]
+    pairs = [(0, 1), (1, 2), (3, 4), (4, 5), (0, 5)]
+    serial = [eng.align_fused(b, pairs)[1].clone() for b in batches]
+    out = [None, None]
+
+    def run(i):
+        s = cuda.cuda.Stream()
+        with cuda.cuda.stream(s):
+            for _ in range(5):
+                _, acc, _ = eng.align_fused(batches[i], pairs)
+            out[i] = acc.clone()
+        s.synchronize()
+
+    ts = [threading.Thread(target=run, args=(i,)) for i in range(2)]
+    for t in ts:
+        t.start()
+    for t in ts:
+        t.join()
+    for i in range(2):
+        assert cuda.equal(out[i], serial[i])
