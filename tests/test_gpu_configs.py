@@ -340,3 +340,34 @@ def test_concurrent_fused_calls_on_two_streams(mtb, cuda):
         t.join()
     for i in range(2):
         assert cuda.equal(out[i], serial[i])
+
+
+def test_random_geometry_sweep_vs_oracle(mtb, cuda):
+    """24 seeded random cases through the public API (align_stack /
+    align(mode="pivot")): widths 16..2600 (multiples of 16 take the fused
+    path at >= 4 MP-equivalent batches only when large, else staged), odd and
+    even heights, 1..6 levels, tolerances 0..200; every pairwise offset, every
+    trace's 9 counts and the aligned outputs equal the oracle's."""
+    rng = np.random.default_rng(20261017)
+    for case in range(24):
+        w = int(rng.integers(16, 2600))
+        if case % 3 == 0:
+            w = max(16, w - w % 16)                     # TMA-friendly width
+        h = int(rng.integers(16, 1700))
+        levels = int(rng.integers(1, 7))
+        tol = int(rng.choice([0, 1, 4, 7, 31, 127, 128, 200]))
+        count = int(rng.integers(2, 5))
+        base = np.dstack([orc.smooth_gray(rng, w, h, cells=6) for _ in range(3)])
+        imgs, _ = orc.generate_stack(base, count, seed=case, max_shift=min(12, max(1, min(w, h) // 8)))
+        mode = "pivot" if case % 2 else "chain"
+        aligned, rec = mtb.align(imgs, levels=levels, tol=tol, mode=mode)
+        if mode == "chain":
+            want_al, want_res, want_cum = orc.align_stack(imgs, levels, tol)
+        else:
+            want_al, want_res, want_cum = orc.align_pivot(imgs, count // 2, levels, tol)
+        assert [tuple(c) for c in rec.cumulative] == [tuple(c) for c in want_cum], (case, w, h, levels, tol)
+        for res, want in zip(rec.pairwise, want_res):
+            for t, wt in zip(res.traces, want["traces"]):
+                assert [e for _, e in t.candidates] == [e for _, e in wt["candidates"]], (case, t.level)
+        for a, b in zip(aligned, want_al):
+            assert np.array_equal(np.asarray(a), b), case
