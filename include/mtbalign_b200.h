@@ -203,6 +203,23 @@ int mtb_threshold_levels(const uint8_t* gray, const uint32_t* hist_ws, int w, in
                          int levels, int tol, uint32_t* hist_out, int32_t* medians,
                          uint64_t* mtb, uint64_t* exclusion, int discard_gray, void* stream);
 
+/* mtb_preprocess for small images without a gray arena (csrc/cluster.cu): the
+ * gray pyramid of each image is held in the shared memory of a thread-block
+ * cluster, so HBM sees only the RGB read and the bitmap writes.  Same outputs
+ * (medians [img][n], optional dense histograms [img][n][256], packed maps) as
+ * mtb_preprocess.  Needs n <= 6 levels, 3*w % 4 == 0, 16-byte aligned rows and
+ * images, and an image whose tiles fit one cluster (about 1.5 MP); otherwise
+ * MTB_EINVAL.  mtb_preprocess_maps_cluster returns the cluster size it would
+ * use on the current device (0 = geometry not supported). */
+int mtb_preprocess_maps(const uint8_t* rgb, int64_t rgb_pitch, int64_t rgb_img_stride,
+                        int w, int h, int n_img, int levels, int tol,
+                        uint32_t* hist_out, int32_t* medians, uint64_t* mtb, uint64_t* exclusion, void* stream);
+int mtb_preprocess_maps_cluster(int w, int h, int levels);
+/* The full launch shape: shape[4] = {cluster size, streaming groups of 128
+ * threads, tile slots per CTA, clusters the device co-schedules}; returns the
+ * cluster size (0 = not supported). */
+int mtb_preprocess_maps_shape(int w, int h, int levels, int* shape);
+
 /* Coarse-to-fine search (find_offset, search.py:74-95; per level
  * search_level, search.py:53-71) for P pairs at once, all levels on device.
  *   maps     device table, n_levels x P x 4 pointers {ref.mtb, ref.excl,

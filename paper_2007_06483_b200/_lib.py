@@ -51,6 +51,8 @@ SIGNATURES = {
                              _c_void_p, _c_void_p, _i32, _c_void_p],
     "mtb_preprocess": [_c_void_p, _i64, _i64, _i32, _i32, _i32, _i32, _i32, _c_void_p, _c_void_p, _c_void_p,
                        _c_void_p, _c_void_p, _c_void_p, _c_void_p],
+    "mtb_preprocess_maps": [_c_void_p, _i64, _i64, _i32, _i32, _i32, _i32, _i32, _c_void_p, _c_void_p,
+                            _c_void_p, _c_void_p, _c_void_p],
     "mtb_find_offset_batch": [_c_void_p, _c_void_p, _i32, _i32, _c_void_p, _c_void_p, _c_void_p, _c_void_p,
                               _c_void_p],
     "mtb_search_level_rows": [_c_void_p, _i32, _i32, _i64, _i32, _i32, _i32, _i32, _i32, _c_void_p, _i64,
@@ -79,6 +81,8 @@ AUX_SIGNATURES = {
     "mtb_align_fused_sync_words": ([_i32, _i32, _i32], ctypes.c_int64),
     "mtb_align_fused_images_per_launch": ([_i32, _i32], ctypes.c_int),
     "mtb_align_fused_launches": ([_i32, _i32, _i32, _i32, _c_void_p, _i32], ctypes.c_int),
+    "mtb_preprocess_maps_cluster": ([_i32, _i32, _i32], ctypes.c_int),
+    "mtb_preprocess_maps_shape": ([_i32, _i32, _i32, _c_void_p], ctypes.c_int),
 }
 
 _lock = threading.Lock()
@@ -100,11 +104,13 @@ def load(path: str = LIB_PATH) -> ctypes.CDLL:
                 f"CUDA engine library not built: {path} is missing; run "
                 "`python -c 'import __graft_entry__ as g; g.build()'` (no CPU fallback exists)")
         lib = ctypes.CDLL(path)
-        for name, argtypes in SIGNATURES.items():
-            fn = getattr(lib, name)
-            fn.argtypes = argtypes
-            fn.restype = ctypes.c_int
-        for name, (argtypes, restype) in AUX_SIGNATURES.items():
+        # an experiment build (MTB_LIB_PATH, tools/ab.sh) may predate newer entry points
+        lenient = bool(os.environ.get("MTB_LIB_PATH"))
+        sigs = [(n, a, ctypes.c_int) for n, a in SIGNATURES.items()] + \
+               [(n, a, r) for n, (a, r) in AUX_SIGNATURES.items()]
+        for name, argtypes, restype in sigs:
+            if lenient and not hasattr(lib, name):
+                continue
             fn = getattr(lib, name)
             fn.argtypes = argtypes
             fn.restype = restype

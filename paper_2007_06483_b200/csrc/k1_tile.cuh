@@ -231,8 +231,15 @@ __device__ __forceinline__ void st8(uint8_t* p, uint32_t a, uint32_t b, uint64_t
   asm volatile("st.global.L2::cache_hint.v2.u32 [%0], {%1, %2}, %3;" ::"l"(p), "r"(a), "r"(b), "l"(pol) : "memory");
 }
 
-// k1_block for the tile-major layout: `tg` = this tile's gray region.
-template <bool FULL>
+// Shared-memory variant of st8 (SMEM tile-major slots, csrc/cluster.cu).
+__device__ __forceinline__ void sts8(uint8_t* p, uint32_t a, uint32_t b) {
+  asm volatile("st.shared.v2.u32 [%0], {%1, %2};" ::"r"(smem_addr(p)), "r"(a), "r"(b) : "memory");
+}
+
+// k1_block for the tile-major layout: `tg` = this tile's gray region (global,
+// or shared memory when SMEM; l3_slot is unused then: level 3 is read back
+// from tg).
+template <bool FULL, bool SMEM = false>
 __device__ __forceinline__ void k1_block_tm(const K1Args& a, uint8_t* tg, const uint2 (&v)[8][3], int tx, int ty,
                                             int wg, int lane, uint32_t hb, uint8_t* l3_slot, uint64_t gpol) {
   const int x0 = tx * kK1TilePx + 8 * lane;
@@ -257,7 +264,10 @@ __device__ __forceinline__ void k1_block_tm(const K1Args& a, uint8_t* tg, const 
           if (FULL || (row_ok && i < nv0)) hinc(hb | ((sa[i] >> 6) & 0x3fcu));
           if (FULL || (row_ok && 4 + i < nv0)) hinc(hb | ((sb[i] >> 6) & 0x3fcu));
         }
-        st8(p0 + r * tm_pitch(0), gw[j][0], gw[j][1], gpol);
+        if constexpr (SMEM)
+          sts8(p0 + r * tm_pitch(0), gw[j][0], gw[j][1]);
+        else
+          st8(p0 + r * tm_pitch(0), gw[j][0], gw[j][1], gpol);
       }
       if (a.nl >= 2) {
         const uint32_t s0 = box_sum(gw[0][0], gw[1][0], 0), s1 = box_sum(gw[0][0], gw[1][0], 1);
@@ -270,6 +280,8 @@ __device__ __forceinline__ void k1_block_tm(const K1Args& a, uint8_t* tg, const 
         if (FULL || (row_ok && 3 < nv1)) hinc(hb1 | (s3 & 0x3fcu));
         const uint32_t x01 = (s0 + (s1 << 16)) >> 2, x23 = (s2 + (s3 << 16)) >> 2;
         l1[rp] = __byte_perm(x01, x23, 0x6420);
+        if constexpr (SMEM)   // (the global layout re-derives level 1 from level 0 in K3)
+          *reinterpret_cast<uint32_t*>(tg + tm_off(1) + (4 * wg + rp) * tm_pitch(1) + 4 * lane) = l1[rp];
       }
     }
   }
@@ -295,7 +307,7 @@ __device__ __forceinline__ void k1_block_tm(const K1Args& a, uint8_t* tg, const 
     const int x3 = x0 >> 3, y3 = y0 >> 3;
     const uint32_t s = box_sum(l2[0], l2[1], 0);
     const uint32_t v3 = s >> 2;
-    *l3_slot = (uint8_t)v3;
+    if constexpr (!SMEM) *l3_slot = (uint8_t)v3;
     tg[tm_off(3) + wg * tm_pitch(3) + lane] = (uint8_t)v3;
     if (FULL || (x3 < a.lw[3] && y3 < a.lh[3])) hinc((hb + 3072) | (s & 0x3fcu));
   }

@@ -149,13 +149,13 @@ struct SearchSmem {
   int last;
 };
 
+// One 64 x 32-word tile of pair p's level (base offset bx, by): returns, for
+// threads 0..8, the tile's error count of candidate tid (0 for the others).
 template <bool SEG>
-__global__ void __launch_bounds__(kSTThreads)
-level_search_kernel(LevelSearchArgs a) {
-  __shared__ SearchSmem S;
-  const int p = blockIdx.y;
+__device__ __forceinline__ unsigned long long search_tile(const LevelSearchArgs& a, SearchSmem& S, int p, int tile,
+                                                          int bx, int by) {
   const int tid = threadIdx.x, lane = tid & 31, wi = tid >> 5;
-  const int tx = blockIdx.x % a.tiles_x, ty = blockIdx.x / a.tiles_x;
+  const int tx = tile % a.tiles_x, ty = tile / a.tiles_x;
   const int ly0 = ty * kSTRows, j0 = tx * kSTWords;   // local (reference-window) row of the tile
   const int y0 = a.a_row0 + ly0;                       // image row of the tile
   const uint32_t* A = SEG ? a.a_m : reinterpret_cast<const uint32_t*>(a.maps[4 * p + 0]);
@@ -163,14 +163,6 @@ level_search_kernel(LevelSearchArgs a) {
   const uint32_t* B = SEG ? nullptr : reinterpret_cast<const uint32_t*>(a.maps[4 * p + 2]);
   const uint32_t* EB = SEG ? nullptr : reinterpret_cast<const uint32_t*>(a.maps[4 * p + 3]);
 
-  int bx = 0, by = 0;
-  if (a.prev) {
-    bx = 2 * a.prev[p * a.prev_stride];
-    by = 2 * a.prev[p * a.prev_stride + 1];
-  } else if (a.base) {
-    bx = a.base[2 * p];
-    by = a.base[2 * p + 1];
-  }
   const int qb = bx >> 5;
   const int sy0 = y0 - by - 1;           // first staged source row
   const int64_t sj0 = (int64_t)j0 - qb - 2;  // first staged source word
@@ -293,13 +285,31 @@ level_search_kernel(LevelSearchArgs a) {
     if (lane == 0) S.part[wi][i] = v;
   }
   __syncthreads();
-  unsigned long long* errs = a.errs + p * a.errs_stride;
+  unsigned long long v = 0;
   if (tid < 9) {
-    unsigned long long v = 0;
 #pragma unroll
     for (int k = 0; k < kSTWarps; ++k) v += S.part[k][tid];
-    if (v) atomicAdd(&errs[tid], v);
   }
+  return v;
+}
+
+template <bool SEG>
+__global__ void __launch_bounds__(kSTThreads)
+level_search_kernel(LevelSearchArgs a) {
+  __shared__ SearchSmem S;
+  const int p = blockIdx.y;
+  const int tid = threadIdx.x;
+  int bx = 0, by = 0;
+  if (a.prev) {
+    bx = 2 * a.prev[p * a.prev_stride];
+    by = 2 * a.prev[p * a.prev_stride + 1];
+  } else if (a.base) {
+    bx = a.base[2 * p];
+    by = a.base[2 * p + 1];
+  }
+  const unsigned long long v = search_tile<SEG>(a, S, p, blockIdx.x, bx, by);
+  unsigned long long* errs = a.errs + p * a.errs_stride;
+  if (tid < 9 && v) atomicAdd(&errs[tid], v);
   if (!a.decide) return;
   __threadfence();
   __syncthreads();
@@ -318,6 +328,61 @@ level_search_kernel(LevelSearchArgs a) {
     }
     a.acc[p * a.acc_stride] = bx + best % 3 - 1;
     a.acc[p * a.acc_stride + 1] = by + best / 3 - 1;
+  }
+}
+
+// The coarse levels of find_offset for one pair per CTA (search.py:74-95):
+// levels n-1 .. k_lo, each a loop over its few tiles, the decision kept on
+// chip and fed to the next level as its base; replaces one launch (and one
+// grid of a handful of CTAs per pair) per coarse level.
+struct PairSearchArgs {
+  const uint64_t* const* maps;   // table [level][P][4]
+  int w[kMaxLevels], h[kMaxLevels], nw32[kMaxLevels];
+  int n_levels, k_lo, P;
+  const int32_t* base;           // [P][2] or nullptr
+  int32_t* acc;                  // [P][n][2]
+  unsigned long long* errs;      // [P][n][9]
+};
+
+__global__ void __launch_bounds__(kSTThreads, 3) pair_search_kernel(PairSearchArgs pa) {
+  __shared__ SearchSmem S;
+  __shared__ unsigned long long s_e[9];
+  __shared__ int s_b[2];
+  const int p = blockIdx.x, tid = threadIdx.x, n = pa.n_levels;
+  int bx = pa.base ? pa.base[2 * p] : 0, by = pa.base ? pa.base[2 * p + 1] : 0;
+  for (int k = n - 1; k >= pa.k_lo; --k) {
+    LevelSearchArgs a{};
+    a.maps = pa.maps + (int64_t)k * pa.P * 4;
+    a.w = pa.w[k];
+    a.h = pa.h[k];
+    a.nw32 = pa.nw32[k];
+    a.a_rows = a.b_rows = a.h;
+    a.tiles_x = (a.nw32 + kSTWords - 1) / kSTWords;
+    const int tiles = a.tiles_x * ((a.h + kSTRows - 1) / kSTRows);
+    unsigned long long tot = 0;
+    for (int t = 0; t < tiles; ++t) tot += search_tile<false>(a, S, p, t, bx, by);
+    if (tid < 9) {
+      s_e[tid] = tot;
+      pa.errs[((int64_t)p * n + k) * 9 + tid] = tot;
+    }
+    __syncthreads();
+    if (tid == 0) {
+      int best = 0;
+      unsigned long long be = 0;
+      int bd = 0;
+#pragma unroll
+      for (int i = 0; i < 9; ++i) {
+        const int d = abs(i % 3 - 1) + abs(i / 3 - 1);
+        if (i == 0 || key_less(s_e[i], d, i, be, bd, best)) { best = i; be = s_e[i]; bd = d; }
+      }
+      s_b[0] = bx + best % 3 - 1;
+      s_b[1] = by + best / 3 - 1;
+      pa.acc[((int64_t)p * n + k) * 2] = s_b[0];
+      pa.acc[((int64_t)p * n + k) * 2 + 1] = s_b[1];
+    }
+    __syncthreads();
+    bx = 2 * s_b[0];
+    by = 2 * s_b[1];
   }
 }
 
@@ -434,7 +499,36 @@ extern "C" int mtb_find_offset_batch(const uint64_t* const* maps, const int32_t*
   MTB_CUDA(cudaMemsetAsync(errs, 0, sizeof(unsigned long long) * 9 * n_levels * P, st));
   MTB_CUDA(cudaMemsetAsync(done, 0, sizeof(uint32_t) * n_levels * P, st));
   int launches = 0;
-  for (int k = n_levels - 1; k >= 0; --k) {
+  // Coarse levels with few tiles: one CTA per pair runs them back to back
+  // (pair_search_kernel); with few pairs only the single-tile levels, so the
+  // serial per-pair loop never replaces a wide grid.
+  const int max_tiles = P >= 64 ? 8 : 2;
+  int k_lo = n_levels;
+  while (k_lo > 0) {
+    const int k = k_lo - 1;
+    const int nw32 = 2 * dims[3 * k + 2];
+    const int tiles = ((nw32 + kSTWords - 1) / kSTWords) * ((dims[3 * k + 1] + kSTRows - 1) / kSTRows);
+    if (tiles > max_tiles) break;
+    k_lo = k;
+  }
+  if (k_lo < n_levels) {
+    PairSearchArgs pa{};
+    pa.maps = maps;
+    for (int k = 0; k < n_levels; ++k) {
+      pa.w[k] = dims[3 * k];
+      pa.h[k] = dims[3 * k + 1];
+      pa.nw32[k] = 2 * dims[3 * k + 2];
+    }
+    pa.n_levels = n_levels;
+    pa.k_lo = k_lo;
+    pa.P = P;
+    pa.base = base;
+    pa.acc = acc;
+    pa.errs = errs;
+    pair_search_kernel<<<P, kSTThreads, 0, st>>>(pa);
+    ++launches;
+  }
+  for (int k = k_lo - 1; k >= 0; --k) {
     LevelSearchArgs a{};
     a.maps = maps + (int64_t)k * P * 4;
     a.w = dims[3 * k];

@@ -18,7 +18,9 @@ struct ThreshLevel {
   int64_t gray_off, gray_pitch;  // bytes (pitch is a multiple of 128)
   int64_t bit_off;               // u64 words
   int nw32;                      // u32 words per packed row
-  int row_begin;                 // first flat row of this level (levels concatenated)
+  int chunks;                    // wide level (nw32 >= 32): ceil(nw32 / 32) warp items per row; 0: narrow
+  uint32_t magic;                // narrow level: ceil(2^32 / nw32) (row = umulhi(word, magic))
+  int item_begin;                // first warp item of this level (levels concatenated)
 };
 
 struct ThreshArgs {
@@ -28,7 +30,7 @@ struct ThreshArgs {
   int tol;
   int n;
   ThreshLevel lv[kMaxLevels];
-  int rows_per_img;              // sum over levels of h
+  int items;                     // warp items per image: sum over levels of h * chunks
   uint32_t* mtb;                 // bitmap arena (u32 view), image stride bit_img_words*2
   uint32_t* excl;
   int64_t bit_img_words32;
@@ -51,46 +53,81 @@ __device__ __forceinline__ void pack32(const uint32_t (&g)[8], int valid, int me
   eb = e & keep;
 }
 
-// One warp per packed row (rows of all levels concatenated); lane j handles
-// words j, j+32, ... of the row, i.e. 32 pixels = 32 aligned gray bytes each.
-__global__ void __launch_bounds__(256) threshold_levels_kernel(ThreshArgs a) {
+// A warp item = 32 packed words (one per lane, 32 gray bytes each): 32
+// consecutive words of one row of a wide level (>= 32 words per row), or 32
+// consecutive words of a narrow level's row-major word sequence (several
+// rows, so no lane idles); the items of all levels are concatenated and the
+// warps of an image's CTAs stride over them.  The per-level compare
+// constants are built once per CTA in shared memory and the pack is the
+// VABSDIFF4 / carry-majority form of the fused pipeline (th_word_t, about 7
+// instructions per 4 pixels), so an item costs little beyond its bytes.
+#ifndef TH_MIN_BLOCKS
+#define TH_MIN_BLOCKS 1
+#endif
+__global__ void __launch_bounds__(256, TH_MIN_BLOCKS) threshold_levels_kernel(ThreshArgs a) {
+  __shared__ ThConst s_th[kMaxLevels];
   const int img = blockIdx.y;
+  if (threadIdx.x < a.n) {
+    const int med = a.medians[img * a.n + threadIdx.x];
+    ThConst c;
+    c.med = (uint32_t)med * 0x01010101u;
+    c.ym = (uint32_t)(255 - med) * 0x01010101u;
+    c.yml = c.ym & 0x7f7f7f7fu;
+    c.med_lo = med <= 127;
+    s_th[threadIdx.x] = c;
+  }
+  __syncthreads();
+  const bool tol_lo = a.tol <= 127;
+  const uint32_t yt = (uint32_t)(255 - a.tol) * 0x01010101u, ytl = yt & 0x7f7f7f7fu;
   const int lane = threadIdx.x & 31;
   const uint8_t* gray = a.gray + img * a.gray_img_stride;
   uint32_t* mtb = a.mtb + img * a.bit_img_words32;
   uint32_t* excl = a.excl + img * a.bit_img_words32;
   const int wpc = blockDim.x >> 5;
-  for (int row = blockIdx.x * wpc + (threadIdx.x >> 5); row < a.rows_per_img; row += gridDim.x * wpc) {
-    int k = 0;
-    while (k + 1 < a.n && row >= a.lv[k + 1].row_begin) ++k;
+  const int stride = gridDim.x * wpc;
+  int k = 0;
+  for (int it = blockIdx.x * wpc + (threadIdx.x >> 5); it < a.items; it += stride) {
+    while (k + 1 < a.n && it >= a.lv[k + 1].item_begin) ++k;   // items only increase
     const ThreshLevel& L = a.lv[k];
-    const int y = row - L.row_begin;
-    const int med = a.medians[img * a.n + k];
-    const int lo = med - a.tol;
-    const GtConst kmed = gt_const(med), khi = gt_const(med + a.tol), klo = gt_const(lo - 1);
-    const uint32_t lomask = lo > 0 ? 0x80808080u : 0u;
-    const uint8_t* grow = gray + L.gray_off + (int64_t)y * L.gray_pitch;
-    uint32_t* mrow = mtb + 2 * L.bit_off + (int64_t)y * L.nw32;
-    uint32_t* erow = excl + 2 * L.bit_off + (int64_t)y * L.nw32;
-    for (int j = lane; j < L.nw32; j += 32) {
-      const int x0 = 32 * j;
-      uint32_t mw = 0, ew = 0;
-      if (x0 < L.w) {
-        // gray pitch is a multiple of 128 bytes: these 32 bytes are in-bounds and aligned.
-        const uint4* p = reinterpret_cast<const uint4*>(grow + x0);
-        const uint4 v0 = __ldcs(p), v1 = __ldcs(p + 1);
-        const uint32_t g[8] = {v0.x, v0.y, v0.z, v0.w, v1.x, v1.y, v1.z, v1.w};
-        pack32_swar(g, L.w - x0, kmed, khi, klo, lomask, mw, ew);
-        if (a.discard) {
-          // words j..j+3 share one 128-B line and are lanes of this iteration;
-          // drop the line from L2 (no write-back) once all of them read it.
-          __syncwarp(__activemask());
-          if ((j & 3) == 0) asm volatile("discard.global.L2 [%0], 128;" ::"l"(grow + x0) : "memory");
-        }
-      }
-      mrow[j] = mw;
-      erow[j] = ew;
+    const int rem = it - L.item_begin;
+    int y, j;
+    if (L.chunks) {          // wide: an item is 32 words of one row
+      y = L.chunks == 1 ? rem : rem / L.chunks;
+      j = (rem - y * L.chunks) * 32 + lane;
+      if (j >= L.nw32) continue;
+    } else {                 // narrow: an item is 32 consecutive words of the level (several rows)
+      const int f = rem * 32 + lane;
+      y = (int)__umulhi((uint32_t)f, L.magic);
+      j = f - y * L.nw32;
+      if (y >= L.h) continue;
     }
+    const int x0 = 32 * j;
+    uint32_t mw = 0, ew = 0;
+    if (x0 < L.w) {
+      // gray pitch is a multiple of 128 bytes: these 32 bytes are in-bounds and aligned.
+      const uint8_t* src = gray + L.gray_off + (int64_t)y * L.gray_pitch + x0;
+      const uint4* p = reinterpret_cast<const uint4*>(src);
+      const uint4 v0 = __ldcs(p), v1 = __ldcs(p + 1);
+      const uint32_t g[8] = {v0.x, v0.y, v0.z, v0.w, v1.x, v1.y, v1.z, v1.w};
+      const ThConst c = s_th[k];
+      if (c.med_lo) {
+        if (tol_lo) th_word_t<true, true>(g, c, yt, ytl, L.w - x0, mw, ew);
+        else th_word_t<true, false>(g, c, yt, ytl, L.w - x0, mw, ew);
+      } else {
+        if (tol_lo) th_word_t<false, true>(g, c, yt, ytl, L.w - x0, mw, ew);
+        else th_word_t<false, false>(g, c, yt, ytl, L.w - x0, mw, ew);
+      }
+      if (a.discard && L.chunks) {
+        // wide level: words j..j+3 share one 128-B line and are lanes of this
+        // item; drop the line from L2 (no write-back) once all of them read it
+        // (narrow levels keep theirs: a row's line may span two items).
+        __syncwarp(__activemask());
+        if ((j & 3) == 0) asm volatile("discard.global.L2 [%0], 128;" ::"l"(src) : "memory");
+      }
+    }
+    const int64_t o = 2 * L.bit_off + (int64_t)y * L.nw32 + j;
+    mtb[o] = mw;
+    excl[o] = ew;
   }
 }
 
@@ -172,7 +209,7 @@ int launch_threshold_levels(const uint8_t* gray, const Plan& p, int n_img, const
   a.medians = medians;
   a.tol = tol;
   a.n = p.n;
-  int rows = 0;
+  int items = 0;
   for (int k = 0; k < p.n; ++k) {
     ThreshLevel& L = a.lv[k];
     L.w = p.lv[k].w;
@@ -181,17 +218,19 @@ int launch_threshold_levels(const uint8_t* gray, const Plan& p, int n_img, const
     L.gray_pitch = p.lv[k].gray_pitch;
     L.bit_off = p.lv[k].bit_off;
     L.nw32 = (int)(2 * p.lv[k].nw64);
-    L.row_begin = rows;
-    rows += L.h;
+    L.chunks = L.nw32 >= 32 ? (L.nw32 + 31) / 32 : 0;
+    L.magic = (uint32_t)((((uint64_t)1 << 32) + L.nw32 - 1) / L.nw32);   // exact for f < 2^32 / nw32
+    L.item_begin = items;
+    items += L.chunks ? L.h * L.chunks : (L.h * L.nw32 + 31) / 32;
   }
-  a.rows_per_img = rows;
+  a.items = items;
   a.mtb = reinterpret_cast<uint32_t*>(mtb);
   a.excl = reinterpret_cast<uint32_t*>(excl);
   a.bit_img_words32 = 2 * p.bit_img_words;
   a.discard = discard;
   int64_t per_img = (int64_t)num_sms() * 8 / (n_img > 0 ? n_img : 1);
   if (per_img < 1) per_img = 1;
-  const int64_t need = (rows + 7) / 8;   // 8 warps (rows) per CTA
+  const int64_t need = (items + 7) / 8;   // 8 warps (items) per CTA
   if (per_img > need) per_img = need;
   threshold_levels_kernel<<<dim3((unsigned)per_img, (unsigned)n_img), 256, 0, st>>>(a);
   return check_launch("threshold_levels_kernel");

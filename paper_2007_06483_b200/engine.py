@@ -58,14 +58,17 @@ class MtbEngine:
         self.dims = np.ascontiguousarray(
             np.stack([self.geom[:, 0], self.geom[:, 1], self.geom[:, 4]], axis=1).astype(np.int32))
         self._tables = {}
+        self._maps_cluster = None
 
     # ------------------------------------------------------------ buffers --
-    def alloc(self, n_img: int, keep_hist: bool = False) -> PyramidSet:
+    def alloc(self, n_img: int, keep_hist: bool = False, gray: bool = True) -> PyramidSet:
+        """Arenas for n_img images; gray=False leaves out the gray pyramid and
+        histogram workspaces (enough for preprocess_maps)."""
         t = self.torch
         return PyramidSet(
             n_img=n_img,
-            gray=t.empty((n_img, self.gray_img_bytes), dtype=t.uint8, device="cuda"),
-            hist_ws=t.empty((n_img, self.hist_ws_elems), dtype=t.int32, device="cuda"),
+            gray=t.empty((n_img, self.gray_img_bytes), dtype=t.uint8, device="cuda") if gray else None,
+            hist_ws=t.empty((n_img, self.hist_ws_elems), dtype=t.int32, device="cuda") if gray else None,
             hist=t.empty((n_img, self.n, 256), dtype=t.int32, device="cuda") if keep_hist else None,
             medians=t.empty((n_img, self.n), dtype=t.int32, device="cuda"),
             mtb=t.empty((n_img, self.bit_img_words), dtype=t.int64, device="cuda"),
@@ -87,8 +90,8 @@ class MtbEngine:
         img_bytes = 3 * self.width * self.height
         return dict(
             rgb=(_dev.ptr(rgb) + i0 * img_bytes) if rgb is not None else None,
-            gray=_dev.ptr(pyr.gray) + i0 * self.gray_img_bytes,
-            hist_ws=_dev.ptr(pyr.hist_ws) + i0 * self.hist_ws_elems * 4,
+            gray=(_dev.ptr(pyr.gray) + i0 * self.gray_img_bytes) if pyr.gray is not None else None,
+            hist_ws=(_dev.ptr(pyr.hist_ws) + i0 * self.hist_ws_elems * 4) if pyr.hist_ws is not None else None,
             hist=(_dev.ptr(pyr.hist) + i0 * self.n * 256 * 4) if pyr.hist is not None else None,
             medians=_dev.ptr(pyr.medians) + i0 * self.n * 4,
             mtb=_dev.ptr(pyr.mtb) + i0 * self.bit_img_words * 8,
@@ -119,14 +122,48 @@ class MtbEngine:
                   self.height, count, self.requested_levels, self.tol, p["gray"], p["hist_ws"], p["hist"],
                   p["medians"], p["mtb"], p["excl"], _dev.stream())
 
+    def maps_cluster(self) -> int:
+        """Cluster size of the on-chip preprocess (csrc/cluster.cu) for this
+        geometry on the current device; 0 when the image does not fit one
+        cluster, has more than 6 levels or its rows are not 16-byte multiples
+        (TMA)."""
+        if self._maps_cluster is None:
+            self._maps_cluster = int(_lib.load().mtb_preprocess_maps_cluster(
+                self.width, self.height, self.requested_levels)) if (3 * self.width) % 16 == 0 else 0
+        return self._maps_cluster
+
+    def on_chip_maps(self) -> bool:
+        """True when preprocess(maps_only=True) takes the on-chip kernel: it
+        beats the staged kernels only while an image fits a cluster of <= 2
+        CTAs (about 0.4 MP; measured 1.3-1.7x there, 0.65-0.85x at 4-16 CTAs:
+        DESIGN.md 4.6)."""
+        return 0 < self.maps_cluster() <= 2
+
+    def preprocess_maps(self, rgb, pyr: PyramidSet, i0: int = 0, count: int | None = None):
+        """Medians + packed maps of images [i0, i0+count) without a gray arena:
+        one launch, each image's gray pyramid held in a thread-block cluster's
+        shared memory (requires maps_cluster() > 0)."""
+        count = int(rgb.shape[0]) - i0 if count is None else count
+        p = self._ptrs(rgb, pyr, i0)
+        _lib.call("mtb_preprocess_maps", p["rgb"], 3 * self.width, 3 * self.width * self.height, self.width,
+                  self.height, count, self.requested_levels, self.tol, p["hist"], p["medians"], p["mtb"],
+                  p["excl"], _dev.stream())
+
     def preprocess(self, rgb, pyr: PyramidSet | None = None, keep_hist: bool = False,
-                   count: bool = True) -> PyramidSet:
-        """MTB pyramids of an (N, H, W, 3) CUDA batch (pipeline.py:80-85 fused)."""
+                   count: bool = True, maps_only: bool = False) -> PyramidSet:
+        """MTB pyramids of an (N, H, W, 3) CUDA batch (pipeline.py:80-85 fused).
+
+        maps_only: the gray pyramid is not needed afterwards; small images then
+        take the on-chip cluster kernel (no gray arena is allocated)."""
         self._check_rgb(rgb)
         n_img = int(rgb.shape[0])
+        on_chip = maps_only and self.on_chip_maps()
         if pyr is None:
-            pyr = self.alloc(n_img, keep_hist)
-        self.preprocess_range(rgb, pyr, 0, n_img)
+            pyr = self.alloc(n_img, keep_hist, gray=not on_chip)
+        if on_chip:
+            self.preprocess_maps(rgb, pyr, 0, n_img)
+        else:
+            self.preprocess_range(rgb, pyr, 0, n_img)
         if count:
             counters.bump(PYRAMID_BUILDS, n_img)
             counters.bump(MTB_PYRAMID_BUILDS, n_img)

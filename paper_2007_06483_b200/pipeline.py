@@ -9,18 +9,21 @@ are summed on the device and all outputs are shifted in one launch.
 
 Path selection (`use_fused`): images of >= 4 MP go through the fused
 pipeline (csrc/pipe.cu: preprocess and search of the whole stack in one
-pipelined launch sequence, 15 % faster at 24 MP); smaller ones through the
-staged kernels (one persistent K1 launch over the whole batch wins there:
-config 1 352 K vs 43 K pairs/s).
+pipelined launch sequence, 15 % faster at 24 MP); images whose gray pyramid
+fits the shared memory of a 1- or 2-CTA cluster (about 0.4 MP) through the
+on-chip preprocess (csrc/cluster.cu: one launch over the whole batch, gray
+never in HBM) and the batched search; the sizes between through the staged
+kernels (one persistent K1 launch over the batch).
 
 Stage windows (pipeline.py:74-112) are CUDA events recorded on the stream at
 the stage boundaries, read after ONE synchronisation at the end of the call
 (no device-wide syncs inside it); host time after the last event is added
 to the last stage, so the stages still sum to the call's wall time:
   grayscale  host -> device upload of the stack
-  pyramid    fused gray + pyramid + histograms (staged), or the whole fused
-             pipeline (preprocess, thresholds and search overlap there)
-  threshold  medians + MTB / exclusion packing (staged; 0 in fused mode)
+  pyramid    fused gray + pyramid + histograms (staged), the on-chip
+             preprocess (images <= 0.4 MP: thresholds included), or the whole
+             fused pipeline (preprocess, thresholds and search overlap there)
+  threshold  medians + MTB / exclusion packing (staged; 0 otherwise)
   search     batched find_offset (staged) + readback of offsets and traces
   shift      device prefix sums, batched shift_rgb, download of the outputs
 
@@ -172,6 +175,11 @@ def _run_batch(eng: MtbEngine, batch, pairs, clk: _StageClock):
         _, acc, errs = eng.align_fused(batch, pairs)
         clk.mark()          # pyramid: the whole pipelined sequence
         clk.mark()          # threshold: inside it
+    elif eng.on_chip_maps():
+        pyr = eng.preprocess(batch, maps_only=True)   # one launch, gray kept on chip (csrc/cluster.cu)
+        clk.mark()          # pyramid and threshold: the same kernel
+        clk.mark()
+        acc, errs = eng.search(pyr, pairs)
     else:
         pyr = eng.alloc(n_img)
         eng.pyramid_hist(batch, pyr)
@@ -320,7 +328,7 @@ def get_exp_shift(ref_rgb, tgt_rgb, levels: int = DEFAULT_LEVELS, tol: int = DEF
     if use_fused(eng):
         _, acc, _ = eng.align_fused(batch, [(0, 1)])     # one pipelined launch sequence (csrc/pipe.cu)
     else:
-        pyr = eng.preprocess(batch)
+        pyr = eng.preprocess(batch, maps_only=True)
         acc, _ = eng.search(pyr, [(0, 1)])
     a = acc[0, 0].cpu().numpy()
     return ShiftOffset(int(a[0]), int(a[1]))
@@ -356,7 +364,7 @@ def align_files(paths, levels: int = DEFAULT_LEVELS, tol: int = DEFAULT_NOISE_TO
         batch, _, acc, errs = eng.align_fused_host(host, pairs)
     else:
         batch = host.to("cuda", non_blocking=True)
-        pyr = eng.preprocess(batch)
+        pyr = eng.preprocess(batch, maps_only=True)
         acc, errs = eng.search(pyr, pairs)
     pairwise = results_from_device(acc, errs)
     t2 = time.perf_counter()
