@@ -102,7 +102,7 @@ __global__ void __launch_bounds__(kK1Threads, 1) k1_rgb_pyramid_kernel(K1Args a,
     for (int i = t; i < a.nl * 256; i += kK1GroupThreads) {
       const uint32_t c = gh_s[i];
       if (c) {
-        atomicAdd(&gh[(int64_t)i * kHistStrideK1], c);
+        atomicAdd(&gh[(int64_t)i * a.hist_bin], c);
         gh_s[i] = 0;
       }
     }
@@ -190,7 +190,7 @@ void k1_set_keep_gray(int v) { g_keep_gray = v; }
 // Levels 0..min(n,6)-1 of n_img images in ONE persistent launch (one CTA per
 // SM over the image-major tile sequence).
 int launch_k1_rgb(const uint8_t* rgb, int64_t rgb_pitch, int64_t rgb_img_stride, int n_img, const Plan& p,
-                  uint8_t* gray, uint32_t* spread_hist, int64_t hist_img_stride, cudaStream_t st) {
+                  uint8_t* gray, uint32_t* spread_hist, int64_t hist_img_stride, int hist_bin, cudaStream_t st) {
   K1Args a{};
   a.rgb_pitch = rgb_pitch;
   a.rgb_img_stride = rgb_img_stride;
@@ -210,6 +210,7 @@ int launch_k1_rgb(const uint8_t* rgb, int64_t rgb_pitch, int64_t rgb_img_stride,
     a.lh[k] = k < p.n ? p.lv[k].h : 0;
   }
   a.hist_img_stride = hist_img_stride;
+  a.hist_bin = hist_bin;
   a.keep_gray = g_keep_gray;
   a.tiles_x = (a.w + kK1TilePx - 1) / kK1TilePx;   // edge tiles included: TMA zero-fills outside the image
   a.tiles_y = (a.h + kK1TileRows - 1) / kK1TileRows;

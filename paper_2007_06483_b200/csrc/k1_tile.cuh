@@ -31,8 +31,9 @@ struct K1Args {
   int off[6], pitch[6];     // within-image byte offsets (image gray arena < 2 GB)
   int lw[6], lh[6];
   int nl;                 // levels produced (1..6)
-  uint32_t* hist;         // spread histograms [img][level][bin * 32]
+  uint32_t* hist;         // histograms [img][level][bin * hist_bin]
   int64_t hist_img_stride;
+  int hist_bin;           // u32 stride between bins (32: spread, 1: dense)
   int tiles_x, tiles_y;   // ceil(w/256) x ceil(h/32)
   int n_img;              // images of this launch (tiles are numbered image-major)
   int keep_gray;          // store gray with L2::evict_last (else evict_normal)

@@ -1249,6 +1249,7 @@ extern "C" int mtb_align_fused_ex(const uint8_t* rgb, int64_t rgb_pitch, int64_t
   g.gray_img_stride = slot_bytes;   // tile-major slot (k1_tile.cuh kTmOff)
   g.hist = hist_ws;
   g.hist_img_stride = spread_hist_elems(p.n);
+  g.hist_bin = kHistStrideK1;
   g.tiles_x = (w + kK1TilePx - 1) / kK1TilePx;
   g.tiles_y = (h + kK1TileRows - 1) / kK1TileRows;
   g.n_img = 1;

@@ -36,8 +36,9 @@ struct PyrArgs {
   int64_t pitch[kTileLevels];
   int w[kTileLevels], h[kTileLevels];
   int nl;                             // tile levels produced (t = 0..nl-1), 1..6
-  uint32_t* hist;                     // spread layout: [img][level][bin] * kHistStride
+  uint32_t* hist;                     // [img][level][bin] * hist_bin (spread: kHistStride, dense: 1)
   int64_t hist_img_stride;            // u32 elements
+  int hist_bin;                       // u32 stride between global bins
   int hist_level0;                    // global level index of t = 0
   int tiles_x, tiles_y;
   int edge_only;                      // 1: only the partial right column / bottom row tiles
@@ -224,25 +225,25 @@ pyramid_tiles_kernel(PyrArgs a) {
   uint32_t* gh = a.hist + img * a.hist_img_stride;
   for (int i = t0 * 256 + tid; i < a.nl * 256; i += kPyrThreads) {
     const uint32_t v = s_hist[i];
-    if (v) atomicAdd(&gh[(int64_t)(a.hist_level0 * 256 + i) * kHistStride], v);
+    if (v) atomicAdd(&gh[(int64_t)(a.hist_level0 * 256 + i) * a.hist_bin], v);
   }
 }
 
 // Gather the spread histogram into dense u32 [img][level][256] and take the
 // lower median of each (threshold.py:31-39): one warp per (image, level).
-__global__ void hist_median_kernel(const uint32_t* __restrict__ spread, int64_t spread_img_stride,
+__global__ void hist_median_kernel(const uint32_t* __restrict__ spread, int64_t spread_img_stride, int bin,
                                    int n_levels, uint32_t* __restrict__ dense,
                                    int32_t* __restrict__ medians) {
   const int lane = threadIdx.x & 31;
   const int level = threadIdx.x >> 5;
   const int img = blockIdx.x;
   if (level >= n_levels) return;
-  const uint32_t* src = spread + img * spread_img_stride + (int64_t)level * 256 * kHistStride;
+  const uint32_t* src = spread + img * spread_img_stride + (int64_t)level * 256 * bin;
   uint32_t bins[8];
   unsigned long long s = 0;
 #pragma unroll
   for (int i = 0; i < 8; ++i) {
-    bins[i] = src[(int64_t)(lane * 8 + i) * kHistStride];
+    bins[i] = src[(int64_t)(lane * 8 + i) * bin];
     s += bins[i];
   }
   if (dense) {
@@ -349,23 +350,34 @@ __global__ void median64_kernel(const unsigned long long* __restrict__ hist, int
 // Spread-histogram workspace needed by launch_pyramid (u32 elements / image).
 int64_t spread_hist_elems(int n_levels) { return (int64_t)n_levels * 256 * kHistStride; }
 
+// Bin stride of the staged histograms for one mtb_preprocess call: spread (one
+// 128-B line per bin) when many CTAs flush into one image's histogram, dense
+// when each CTA's tile range covers >= 2 whole images (the flushes of an
+// image then come from a handful of CTAs, and the 32x smaller workspace
+// saves the memset and the median pass ~200 MB per 1024 small images).
+int hist_bin_for(const Plan& p, int n_img) {
+  const int64_t tiles = (int64_t)((p.lv[0].w + 255) / 256) * ((p.lv[0].h + 31) / 32);
+  return (int64_t)n_img * tiles >= 2 * tiles * num_sms() ? 1 : kHistStride;
+}
+
 // Builds gray levels 0..n-1 (plan p) and their spread histograms for n_img
 // images.  Level 0 comes from RGB; deeper levels are produced 6 per pass.
 int launch_k1_rgb(const uint8_t* rgb, int64_t rgb_pitch, int64_t rgb_img_stride, int n_img, const Plan& p,
-                  uint8_t* gray, uint32_t* spread_hist, int64_t hist_img_stride, cudaStream_t st);
+                  uint8_t* gray, uint32_t* spread_hist, int64_t hist_img_stride, int hist_bin, cudaStream_t st);
 bool k1_rgb_supported(int w, int64_t rgb_pitch, int64_t rgb_img_stride, const void* rgb);
 
 // Builds gray levels 0..n-1 (plan p) and their spread histograms for n_img
 // images: levels 0..5 by the fused RGB kernel (k1_rgb.cu), deeper levels by
 // tile passes over the deepest level produced so far (6 levels per pass).
 int launch_pyramid(const uint8_t* rgb, int64_t rgb_pitch, int64_t rgb_img_stride, int n_img,
-                   const Plan& p, uint8_t* gray, uint32_t* spread_hist, cudaStream_t st) {
+                   const Plan& p, uint8_t* gray, uint32_t* spread_hist, int hist_bin, cudaStream_t st) {
+  const int64_t hist_img = (int64_t)p.n * 256 * hist_bin;
   // Interior tiles: the fast kernel (needs 16-B aligned RGB rows).  Edge
   // tiles (and every tile when rows are unaligned): the generic kernel.
   const bool vec_ok = k1_rgb_supported(p.lv[0].w, rgb_pitch, rgb_img_stride, rgb);
   int launches = 0;
   if (vec_ok) {
-    int rc = launch_k1_rgb(rgb, rgb_pitch, rgb_img_stride, n_img, p, gray, spread_hist, spread_hist_elems(p.n), st);
+    int rc = launch_k1_rgb(rgb, rgb_pitch, rgb_img_stride, n_img, p, gray, spread_hist, hist_img, hist_bin, st);
     if (rc) return rc;
   }
   {
@@ -386,7 +398,8 @@ int launch_pyramid(const uint8_t* rgb, int64_t rgb_pitch, int64_t rgb_img_stride
       a.h[t] = t < p.n ? p.lv[l].h : 0;
     }
     a.hist = spread_hist;
-    a.hist_img_stride = spread_hist_elems(p.n);
+    a.hist_img_stride = hist_img;
+    a.hist_bin = hist_bin;
     a.hist_level0 = 0;
     a.tiles_x = (int)((a.src_w + kTileCols - 1) / kTileCols);
     a.tiles_y = (int)((a.src_h + kTileRows - 1) / kTileRows);
@@ -421,7 +434,8 @@ int launch_pyramid(const uint8_t* rgb, int64_t rgb_pitch, int64_t rgb_img_stride
       a.h[t] = s + t < p.n ? p.lv[l].h : 0;
     }
     a.hist = spread_hist;
-    a.hist_img_stride = spread_hist_elems(p.n);
+    a.hist_img_stride = hist_img;
+    a.hist_bin = hist_bin;
     a.hist_level0 = s;
     a.tiles_x = (int)((a.src_w + kTileCols - 1) / kTileCols);
     a.tiles_y = (int)((a.src_h + kTileRows - 1) / kTileRows);
@@ -437,10 +451,10 @@ int launch_pyramid(const uint8_t* rgb, int64_t rgb_pitch, int64_t rgb_img_stride
   return launches ? check_launch("pyramid_tiles_kernel", launches) : MTB_OK;
 }
 
-int launch_hist_median(const uint32_t* spread_hist, int n_img, int n_levels, uint32_t* dense,
+int launch_hist_median(const uint32_t* spread_hist, int n_img, int n_levels, int hist_bin, uint32_t* dense,
                        int32_t* medians, cudaStream_t st) {
-  hist_median_kernel<<<n_img, 32 * n_levels, 0, st>>>(spread_hist, spread_hist_elems(n_levels), n_levels,
-                                                      dense, medians);
+  hist_median_kernel<<<n_img, 32 * n_levels, 0, st>>>(spread_hist, (int64_t)n_levels * 256 * hist_bin, hist_bin,
+                                                      n_levels, dense, medians);
   return check_launch("hist_median_kernel");
 }
 
