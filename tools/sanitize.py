@@ -1,7 +1,9 @@
 """Workload for compute-sanitizer (tools/sanitize.sh): a fused batch of 8
 images (4 K1 launches of 2 images + trailing search launches), chain pairs
 plus a cross-launch pair, then the streamed-input variant (per-image H2D
-flags), then a staged preprocess + search of the same batch."""
+flags), then a staged preprocess + search of the same batch (64 pairs too:
+the per-pair coarse-level search), then the on-chip cluster preprocess
+(csrc/cluster.cu) at its natural cluster size and forced to 8 CTAs."""
 import os
 import sys
 
@@ -24,6 +26,17 @@ host = batch.cpu().pin_memory()
 _, _, acc2, _ = eng.align_fused_host(host, pairs)
 pyr = eng.preprocess(batch)
 acc3, _ = eng.search(pyr, pairs)
+acc64, _ = eng.search(pyr, pairs * 8)
+outs = []
+for forced in (None, "8"):
+    if forced:
+        os.environ["MTB_CM_CLUSTER"] = forced
+    if eng.maps_cluster() or forced:
+        p2 = eng.alloc(8, gray=False)
+        eng.preprocess_maps(batch, p2)
+        outs.append(eng.search(p2, pairs)[0])
+    os.environ.pop("MTB_CM_CLUSTER", None)
 torch.cuda.synchronize()
-assert torch.equal(acc, acc2) and torch.equal(acc, acc3)
-print("ok", acc[:, 0].tolist())
+assert torch.equal(acc, acc2) and torch.equal(acc, acc3) and torch.equal(acc64[:8], acc)
+assert all(torch.equal(o, acc) for o in outs), len(outs)
+print("ok", acc[:, 0].tolist(), "on-chip runs", len(outs))
