@@ -303,6 +303,20 @@ __device__ __forceinline__ void k3_bulk_issue(const PipeArgs& a, const uint8_t* 
   }
 }
 
+// Lanes read their 32-byte word as two 16-byte halves; lanes with bit 2 set
+// read the upper half first so each LDS.128 of a warp touches 8 distinct
+// 16-B bank groups per 128 B (lane stride 32 B otherwise hits only 4: 2-way
+// conflicts).  The pack of swapped halves comes out rotated by 16 bits.
+__device__ __forceinline__ uint32_t keep_mask(int valid) {
+  return valid >= 32 ? 0xffffffffu : (valid <= 0 ? 0u : ((1u << valid) - 1u));
+}
+__device__ __forceinline__ void ld_word_sw(const uint8_t* p, int sw, uint32_t (&g)[8]) {
+  const uint4 v0 = *reinterpret_cast<const uint4*>(p + 16 * sw);
+  const uint4 v1 = *reinterpret_cast<const uint4*>(p + 16 * (sw ^ 1));
+  g[0] = v0.x; g[1] = v0.y; g[2] = v0.z; g[3] = v0.w;
+  g[4] = v1.x; g[5] = v1.y; g[6] = v1.z; g[7] = v1.w;
+}
+
 template <bool MED_LO>
 __device__ __forceinline__ void k3_bulk_units(const PipeArgs& a, uint32_t* mtb, uint32_t* excl, const ThConst& c,
                                               uint32_t yt, uint32_t ytl, int K, int r, int lane, const uint8_t* buf) {
@@ -322,11 +336,14 @@ __device__ __forceinline__ void k3_bulk_units(const PipeArgs& a, uint32_t* mtb, 
     const int row = rem >> lwpr, cc = rem & (wpr - 1);
     const int ty = div_tiles_x(a, t), tx = t - ty * a.g.tiles_x;
     const int y = ty * rows + row, j = tx * wpr + cc;
-    const uint4 v0 = *reinterpret_cast<const uint4*>(buf + w * 32);
-    const uint4 v1 = *reinterpret_cast<const uint4*>(buf + w * 32 + 16);
-    const uint32_t g[8] = {v0.x, v0.y, v0.z, v0.w, v1.x, v1.y, v1.z, v1.w};
+    uint32_t g[8];
+    const int sw = (lane >> 2) & 1;
+    ld_word_sw(buf + w * 32, sw, g);
     uint32_t m, e;
-    th_word_t<MED_LO, true>(g, c, yt, ytl, lw - 32 * j, m, e);
+    th_word_t<MED_LO, true>(g, c, yt, ytl, 32, m, e);
+    const uint32_t keep = keep_mask(lw - 32 * j), rot = 16 * sw;
+    m = __funnelshift_l(m, m, rot) & keep;
+    e = __funnelshift_l(e, e, rot) & keep;
     if (t < ntiles && y < lh && j < nw) {
       const int o = boff + y * nw + j;
       mtb[o] = m;
@@ -349,7 +366,9 @@ __device__ __forceinline__ void k3_bulk_units_l0(const PipeArgs& a, uint32_t* mt
   const int ty = div_tiles_x(a, t), tx = t - ty * a.g.tiles_x;
   const int j = tx * 8 + (lane & 7);
   const int y0 = ty * kK1TileRows + ((r & 1) << 4) + (lane >> 3);
-  const int valid = a.g.lw[0] - 32 * j;
+  const uint32_t keep = keep_mask(a.g.lw[0] - 32 * j);
+  const int sw = (lane >> 2) & 1;
+  const uint32_t rot = 16 * sw;
   const bool ok = j < nw;
   // running pointers: unit i is 4 rows below unit i-1
   uint32_t* pm = mtb + (int)a.bit_off32[0] + y0 * nw + j;
@@ -358,11 +377,12 @@ __device__ __forceinline__ void k3_bulk_units_l0(const PipeArgs& a, uint32_t* mt
   int rows_left = ok ? lh - y0 : 0;
 #pragma unroll kK3L0Unroll
   for (int i = 0; i < kK3Units; ++i) {
-    const uint4 v0 = *reinterpret_cast<const uint4*>(src);
-    const uint4 v1 = *reinterpret_cast<const uint4*>(src + 16);
-    const uint32_t g[8] = {v0.x, v0.y, v0.z, v0.w, v1.x, v1.y, v1.z, v1.w};
+    uint32_t g[8];
+    ld_word_sw(src, sw, g);
     uint32_t m, e;
-    th_word_t<MED_LO, true>(g, c, yt, ytl, valid, m, e);
+    th_word_t<MED_LO, true>(g, c, yt, ytl, 32, m, e);
+    m = __funnelshift_l(m, m, rot) & keep;
+    e = __funnelshift_l(e, e, rot) & keep;
     if (rows_left > 0) {
       *pm = m;
       *pe = e;
@@ -383,11 +403,17 @@ __device__ __forceinline__ void k3_level1_from_l0(const PipeArgs& a, uint32_t* m
                                                   uint32_t yt, uint32_t ytl, int r, int lane, const uint8_t* buf) {
   const int r1 = lane >> 2, c = lane & 3;
   const uint8_t* up = buf + (2 * r1) * kK1TilePx + 64 * c;
+  // Lane (r1, c) reads its four 16-px chunks starting at chunk r1 & 3, so a
+  // warp's LDS.128 covers all 8 bank groups (lanes differ by 512 B per row
+  // and 64 B per column: in order they would share 2 of 8, 16-way).  The
+  // pack then comes out rotated by 8 (r1 & 3) bits.
+  const int q0 = r1 & 3;
   uint32_t g[8];
 #pragma unroll
-  for (int q = 0; q < 4; ++q) {   // 16 L0 px of each row -> 8 L1 px = g[2q], g[2q+1]
-    const uint4 u = *reinterpret_cast<const uint4*>(up + 16 * q);
-    const uint4 d = *reinterpret_cast<const uint4*>(up + kK1TilePx + 16 * q);
+  for (int q = 0; q < 4; ++q) {   // chunk (q0 + q) & 3: 16 L0 px of each row -> 8 L1 px = g[2q], g[2q+1]
+    const int qq = (q0 + q) & 3;
+    const uint4 u = *reinterpret_cast<const uint4*>(up + 16 * qq);
+    const uint4 d = *reinterpret_cast<const uint4*>(up + kK1TilePx + 16 * qq);
     const uint32_t uw[4] = {u.x, u.y, u.z, u.w}, dw[4] = {d.x, d.y, d.z, d.w};
     uint32_t x[4];
 #pragma unroll
@@ -399,7 +425,10 @@ __device__ __forceinline__ void k3_level1_from_l0(const PipeArgs& a, uint32_t* m
   const int ty = div_tiles_x(a, t), tx = t - ty * a.g.tiles_x;
   const int y = ty * (kK1TileRows / 2) + 8 * (r & 1) + r1, j = tx * 4 + c;
   uint32_t m, e;
-  th_word(g, c1, yt, ytl, a.g.lw[1] - 32 * j, m, e);   // generic form: smaller code measured faster here
+  th_word(g, c1, yt, ytl, 32, m, e);   // generic form: smaller code measured faster here
+  const uint32_t keep = keep_mask(a.g.lw[1] - 32 * j), rot = 8 * q0;
+  m = __funnelshift_l(m, m, rot) & keep;
+  e = __funnelshift_l(e, e, rot) & keep;
   if (y < a.g.lh[1] && j < a.nw32[1]) {
     const int o = (int)a.bit_off32[1] + y * a.nw32[1] + j;
     mtb[o] = m;
