@@ -9,6 +9,8 @@
 //   search_level: 9 candidates base + (ddx, ddy), (ddy, ddx) row-major over
 //   {-1,0,1}^2, winner minimises (err, |ddx|+|ddy|, index)   search.py:20-23,53-71
 //   find_offset: deepest level first, base = 2 * previous   search.py:74-95
+#include <type_traits>
+
 #include "common.cuh"
 
 namespace mtb {
@@ -225,37 +227,36 @@ __device__ __forceinline__ unsigned long long search_tile(const LevelSearchArgs&
   __syncthreads();
 
   // ---- compute: warp wi -> output rows 8wi .. 8wi+7, lane -> word ----
-  int o[3], r[3];
-#pragma unroll
-  for (int d = 0; d < 3; ++d) {
-    const int dx = bx + d - 1;
-    o[d] = (dx >> 5) - qb;  // in {-1, 0, 1}
-    r[d] = dx & 31;
-  }
-  // Source row lb (local) shifted by bx-1, bx, bx+1: W[j-q] = w[2-o], W[j-q-1] = w[1-o]
-  // with w[i] = staged word lane + i.
-  auto shifted_row = [&](int lb, uint32_t (&sb)[3], uint32_t (&se)[3]) {
-    uint32_t wb[4], we[4];
-#pragma unroll
-    for (int i = 0; i < 4; ++i) {
-      wb[i] = S.b[lb][lane + i];
-      we[i] = S.eb[lb][lane + i];
-    }
-#pragma unroll
-    for (int d = 0; d < 3; ++d) {
-      const uint32_t hb = o[d] < 0 ? wb[3] : (o[d] == 0 ? wb[2] : wb[1]);
-      const uint32_t lb_ = o[d] < 0 ? wb[2] : (o[d] == 0 ? wb[1] : wb[0]);
-      const uint32_t he = o[d] < 0 ? we[3] : (o[d] == 0 ? we[2] : we[1]);
-      const uint32_t le = o[d] < 0 ? we[2] : (o[d] == 0 ? we[1] : we[0]);
-      sb[d] = shifted_word(lb_, hb, r[d]);
-      se[d] = shifted_word(le, he, r[d]);
-    }
-  };
+  // Candidate dx = bx - 1, bx, bx + 1 reads staged words (lane + 1, lane + 2)
+  // funnel-shifted by (dx & 31), except dx = bx - 1 when bx & 31 == 0 (words
+  // lane + 2, lane + 3) and dx = bx + 1 when bx & 31 == 31 (lane, lane + 1):
+  // three compile-time cases (CTA-uniform), no per-word selects.
   unsigned cnt[9];
 #pragma unroll
   for (int i = 0; i < 9; ++i) cnt[i] = 0;
   const int rbeg = wi * (kSTRows / kSTWarps);
-  if (ly0 + rbeg < a.a_rows) {
+  const int rbx = bx & 31;
+  auto rows = [&](auto case_tag) {
+    constexpr int CASE = decltype(case_tag)::value;   // 0: rbx == 0, 1: rbx == 31, 2: other
+    const int r0 = CASE == 0 ? 31 : (CASE == 1 ? 30 : rbx - 1);
+    const int r1 = CASE == 0 ? 0 : (CASE == 1 ? 31 : rbx);
+    const int r2 = CASE == 0 ? 1 : (CASE == 1 ? 0 : rbx + 1);
+    auto shifted_row = [&](int lb, uint32_t (&sb)[3], uint32_t (&se)[3]) {
+      const uint32_t w0 = S.b[lb][lane], w1 = S.b[lb][lane + 1], w2 = S.b[lb][lane + 2];
+      const uint32_t v0 = S.eb[lb][lane], v1 = S.eb[lb][lane + 1], v2 = S.eb[lb][lane + 2];
+      if (CASE == 0) {
+        const uint32_t w3 = S.b[lb][lane + 3], v3 = S.eb[lb][lane + 3];
+        sb[0] = shifted_word(w2, w3, r0); se[0] = shifted_word(v2, v3, r0);
+      } else {
+        sb[0] = shifted_word(w1, w2, r0); se[0] = shifted_word(v1, v2, r0);
+      }
+      sb[1] = shifted_word(w1, w2, r1); se[1] = shifted_word(v1, v2, r1);
+      if (CASE == 1) {
+        sb[2] = shifted_word(w0, w1, r2); se[2] = shifted_word(v0, v1, r2);
+      } else {
+        sb[2] = shifted_word(w1, w2, r2); se[2] = shifted_word(v1, v2, r2);
+      }
+    };
     // output local row rr needs source local rows rr (ddy=+1), rr+1 (ddy=0), rr+2 (ddy=-1)
     uint32_t b0[3], e0[3], b1[3], e1[3];
     shifted_row(rbeg, b0, e0);
@@ -278,6 +279,11 @@ __device__ __forceinline__ unsigned long long search_tile(const LevelSearchArgs&
         b1[d] = b2[d]; e1[d] = e2[d];
       }
     }
+  };
+  if (ly0 + rbeg < a.a_rows) {
+    if (rbx == 0) rows(std::integral_constant<int, 0>{});
+    else if (rbx == 31) rows(std::integral_constant<int, 1>{});
+    else rows(std::integral_constant<int, 2>{});
   }
 #pragma unroll
   for (int i = 0; i < 9; ++i) {
