@@ -15,6 +15,13 @@
 
 namespace mtb {
 
+// 4-byte global -> shared copy, zero-filled when !ok (src is not read then).
+__device__ __forceinline__ void cp_async4(uint32_t* dst, const uint32_t* src, bool ok) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;" ::"r"((uint32_t)__cvta_generic_to_shared(dst)),
+               "l"(src), "r"(ok ? 4 : 0)
+               : "memory");
+}
+
 // Word idx of a packed row (u32 view), zero outside [0, nw32).
 __device__ __forceinline__ uint32_t row_word(const uint32_t* row, int64_t idx, int nw32) {
   return (idx >= 0 && idx < nw32) ? __ldg(row + idx) : 0u;
@@ -169,60 +176,57 @@ __device__ __forceinline__ unsigned long long search_tile(const LevelSearchArgs&
   const int sy0 = y0 - by - 1;           // first staged source row
   const int64_t sj0 = (int64_t)j0 - qb - 2;  // first staged source word
 
-  // ---- stage (all loads in flight together) ----
-  constexpr int kAPer = kSTRows * kSTWords / kSTThreads;                      // 8
-  constexpr int kBPer = (kSTBRows * kSTBWords + kSTThreads - 1) / kSTThreads;  // 10
-  uint32_t ra[kAPer], rea[kAPer], rb[kBPer], reb[kBPer];
+  // ---- stage: global -> shared by 4-byte cp.async (zero-filled outside the
+  // maps), all copies in flight together.  Warp wi stages rows wi, wi + 8, ...
+  // (row validity and the row pointer are warp-uniform), lane = word; the
+  // target halo's words 32..34 go to lanes 0..2. ----
+  {
+    const int jA = j0 + lane;
+    const bool colA = jA < a.nw32;
 #pragma unroll
-  for (int u = 0; u < kAPer; ++u) {
-    const int i = tid + u * kSTThreads;
-    const int r = i / kSTWords, c = i - r * kSTWords;
-    const int ly = ly0 + r, j = j0 + c;
-    const bool ok = ly < a.a_rows && j < a.nw32;
-    ra[u] = ok ? __ldg(A + (int64_t)ly * a.nw32 + j) : 0u;
-    rea[u] = ok ? __ldg(EA + (int64_t)ly * a.nw32 + j) : 0u;
-  }
+    for (int k = 0; k < kSTRows / kSTWarps; ++k) {
+      const int r = wi + kSTWarps * k, ly = ly0 + r;
+      const bool ok = colA && ly < a.a_rows;
+      const int64_t o = ok ? (int64_t)ly * a.nw32 + jA : 0;
+      cp_async4(&S.a[r][lane], A + o, ok);
+      cp_async4(&S.ea[r][lane], EA + o, ok);
+    }
+    const int64_t jb0 = sj0 + lane, jb1 = sj0 + 32 + lane;
+    const bool cb0 = jb0 >= 0 && jb0 < a.nw32;
+    const bool cb1 = lane < kSTBWords - 32 && jb1 >= 0 && jb1 < a.nw32;
 #pragma unroll
-  for (int u = 0; u < kBPer; ++u) {
-    const int i = tid + u * kSTThreads;
-    const int r = i / kSTBWords, c = i - r * kSTBWords;
-    const int64_t y = (int64_t)sy0 + r, j = sj0 + c;
-    if (SEG) {
+    for (int k = 0; k < (kSTBRows + kSTWarps - 1) / kSTWarps; ++k) {
+      const int r = wi + kSTWarps * k;
+      if (r >= kSTBRows) break;
+      const int64_t y = (int64_t)sy0 + r;
       const uint32_t* pm = nullptr;
       const uint32_t* pe = nullptr;
-      int64_t ry = 0;
+      if (y >= 0 && y < a.h) {
+        if (SEG) {
 #pragma unroll
-      for (int sg = 0; sg < 3; ++sg)
-        if (y >= a.seg_row0[sg] && y < (int64_t)a.seg_row0[sg] + a.seg_rows[sg]) {
-          pm = a.seg_m[sg];
-          pe = a.seg_e[sg];
-          ry = y - a.seg_row0[sg];
+          for (int sg = 0; sg < 3; ++sg)
+            if (a.seg_m[sg] && y >= a.seg_row0[sg] && y < (int64_t)a.seg_row0[sg] + a.seg_rows[sg]) {
+              pm = a.seg_m[sg] + (y - a.seg_row0[sg]) * a.nw32;
+              pe = a.seg_e[sg] + (y - a.seg_row0[sg]) * a.nw32;
+            }
+        } else if (y >= a.b_row0 && y < a.b_row0 + a.b_rows) {
+          pm = B + (y - a.b_row0) * a.nw32;
+          pe = EB + (y - a.b_row0) * a.nw32;
         }
-      const bool ok = i < kSTBRows * kSTBWords && pm != nullptr && y >= 0 && y < a.h && j >= 0 && j < a.nw32;
-      rb[u] = ok ? __ldg(pm + ry * a.nw32 + j) : 0u;
-      reb[u] = ok ? __ldg(pe + ry * a.nw32 + j) : 0u;
-    } else {
-      const bool ok = i < kSTBRows * kSTBWords && y >= 0 && y < a.h && y >= a.b_row0 &&
-                      y < a.b_row0 + a.b_rows && j >= 0 && j < a.nw32;
-      rb[u] = ok ? __ldg(B + (y - a.b_row0) * a.nw32 + j) : 0u;
-      reb[u] = ok ? __ldg(EB + (y - a.b_row0) * a.nw32 + j) : 0u;
+      }
+      const bool row = pm != nullptr;
+      if (!row) {
+        pm = A;
+        pe = EA;
+      }
+      cp_async4(&S.b[r][lane], pm + (row && cb0 ? jb0 : 0), row && cb0);
+      cp_async4(&S.eb[r][lane], pe + (row && cb0 ? jb0 : 0), row && cb0);
+      if (lane < kSTBWords - 32) {
+        cp_async4(&S.b[r][32 + lane], pm + (row && cb1 ? jb1 : 0), row && cb1);
+        cp_async4(&S.eb[r][32 + lane], pe + (row && cb1 ? jb1 : 0), row && cb1);
+      }
     }
-  }
-#pragma unroll
-  for (int u = 0; u < kAPer; ++u) {
-    const int i = tid + u * kSTThreads;
-    const int r = i / kSTWords, c = i - r * kSTWords;
-    S.a[r][c] = ra[u];
-    S.ea[r][c] = rea[u];
-  }
-#pragma unroll
-  for (int u = 0; u < kBPer; ++u) {
-    const int i = tid + u * kSTThreads;
-    if (i < kSTBRows * kSTBWords) {
-      const int r = i / kSTBWords, c = i - r * kSTBWords;
-      S.b[r][c] = rb[u];
-      S.eb[r][c] = reb[u];
-    }
+    asm volatile("cp.async.wait_all;" ::: "memory");
   }
   __syncthreads();
 
