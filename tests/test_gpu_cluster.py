@@ -161,3 +161,29 @@ def test_dispatch_by_cluster_size(mtb, cuda):
     off = mtb.get_exp_shift(imgs[0], imgs[1])
     pre = [orc.preprocess(im, 6, 4) for im in imgs[:2]]
     assert tuple(off) == tuple(orc.find_offset(pre[0]["mtb"], pre[1]["mtb"])["offset"])
+
+
+def test_dense_histograms_match_spread(mtb, cuda):
+    """mtb_preprocess switches to dense staged histograms when each K1 CTA
+    covers >= 2 whole images (n_img >= 2 x SMs); level 6 comes from the
+    tail pyramid pass, which flush with the same stride.  Medians, dense
+    histograms and maps equal the split entry points (spread layout)."""
+    w = h = 1024
+    n = 300
+    eng = mtb.MtbEngine(w, h, 7, 4)
+    assert eng.n == 7
+    batch = _batch(cuda, w, h, 8, 21).repeat(n // 8 + 1, 1, 1, 1)[:n].contiguous()
+    dense = eng.preprocess(batch, keep_hist=True)          # one mtb_preprocess call: dense bins
+    spread = eng.alloc(n, keep_hist=True)
+    eng.pyramid_hist(batch, spread)                         # split calls: spread bins
+    eng.threshold_levels(spread, n)
+    assert cuda.equal(dense.medians, spread.medians)
+    assert cuda.equal(dense.hist, spread.hist)
+    for k in range(eng.n):
+        nw64, off = int(eng.geom[k, 4]), int(eng.geom[k, 5])
+        sl = slice(off, off + nw64 * int(eng.geom[k, 1]))
+        assert cuda.equal(dense.mtb[:, sl], spread.mtb[:, sl]), k
+        assert cuda.equal(dense.excl[:, sl], spread.excl[:, sl]), k
+    host = batch[0].cpu().numpy()
+    want = orc.preprocess(host, 7, 4)
+    assert [lv["median"] for lv in want["mtb"]] == dense.medians[0].tolist()
