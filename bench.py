@@ -81,7 +81,7 @@ def parse():
 # row-sharded) is measured by tools/config5.py, not here.
 CONFIGS = {
     1: {"width": 1024, "height": 768, "units": 512, "stack": 2},
-    2: {"width": 6000, "height": 4000, "units": 32, "stack": 2},
+    2: {"width": 6000, "height": 4000, "units": 64, "stack": 2},
     3: {"width": 6000, "height": 4000, "units": 8, "stack": 7},
     4: {"width": 4000, "height": 3000, "units": 64, "stack": 2},
 }
