@@ -80,10 +80,10 @@ def parse():
 # their middle exposure, 6 pairs each).  Config 5 (one gigapixel pair,
 # row-sharded) is measured by tools/config5.py, not here.
 CONFIGS = {
-    1: {"width": 1024, "height": 768, "units": 512, "stack": 2},
+    1: {"width": 1024, "height": 768, "units": 1024, "stack": 2},
     2: {"width": 6000, "height": 4000, "units": 64, "stack": 2},
-    3: {"width": 6000, "height": 4000, "units": 8, "stack": 7},
-    4: {"width": 4000, "height": 3000, "units": 64, "stack": 2},
+    3: {"width": 6000, "height": 4000, "units": 16, "stack": 7},
+    4: {"width": 4000, "height": 3000, "units": 128, "stack": 2},
 }
 
 
