@@ -503,7 +503,9 @@ __device__ __forceinline__ void th_gather45(const PipeArgs& a, const uint8_t* sl
   for (int q = 0; q < nq; ++q) {
     const int tx = nq * r.j + q;
     uint32_t w4[4] = {0, 0, 0, 0};
-    if (tx < a.g.tiles_x) {
+    // (a unit's last words may lie below the level: r.out < 0, nothing is
+    // stored, and the tile row would be past the slot)
+    if (tx < a.g.tiles_x && r.out >= 0) {
       const uint8_t* p = slot + (int64_t)(ty * a.g.tiles_x + tx) * kTileGrayBytes + tm_off(K) + row * tm_pitch(K);
       if (tw == 16) {
         const uint4 v = *reinterpret_cast<const uint4*>(p);
