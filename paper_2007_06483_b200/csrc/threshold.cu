@@ -18,7 +18,7 @@ struct ThreshLevel {
   int64_t gray_off, gray_pitch;  // bytes (pitch is a multiple of 128)
   int64_t bit_off;               // u64 words
   int nw32;                      // u32 words per packed row
-  int chunks;                    // wide level (nw32 >= 32): ceil(nw32 / 32) warp items per row; 0: narrow
+  int chunks;                    // wide level (nw32 >= 32): 1 (one warp item per row); 0: narrow
   uint32_t magic;                // narrow level: ceil(2^32 / nw32) (row = umulhi(word, magic))
   int item_begin;                // first warp item of this level (levels concatenated)
 };
@@ -53,16 +53,15 @@ __device__ __forceinline__ void pack32(const uint32_t (&g)[8], int valid, int me
   eb = e & keep;
 }
 
-// A warp item = 32 packed words (one per lane, 32 gray bytes each): 32
-// consecutive words of one row of a wide level (>= 32 words per row), or 32
-// consecutive words of a narrow level's row-major word sequence (several
-// rows, so no lane idles); the items of all levels are concatenated and the
-// warps of an image's CTAs stride over them.  The per-level compare
+// A warp item = one row of a wide level (>= 32 words per row; lane j packs
+// words j, j + 32, ...), or 32 consecutive words of a narrow level's
+// row-major word sequence (several rows, so no lane idles); the items of all
+// levels are concatenated and the warps of an image's CTAs stride over them.  The per-level compare
 // constants are built once per CTA in shared memory and the pack is the
 // VABSDIFF4 / carry-majority form of the fused pipeline (th_word_t, about 7
 // instructions per 4 pixels), so an item costs little beyond its bytes.
 #ifndef TH_MIN_BLOCKS
-#define TH_MIN_BLOCKS 1
+#define TH_MIN_BLOCKS 8
 #endif
 __global__ void __launch_bounds__(256, TH_MIN_BLOCKS) threshold_levels_kernel(ThreshArgs a) {
   __shared__ ThConst s_th[kMaxLevels];
@@ -86,40 +85,27 @@ __global__ void __launch_bounds__(256, TH_MIN_BLOCKS) threshold_levels_kernel(Th
   const int wpc = blockDim.x >> 5;
   const int stride = gridDim.x * wpc;
   int k = 0;
-  for (int it = blockIdx.x * wpc + (threadIdx.x >> 5); it < a.items; it += stride) {
-    while (k + 1 < a.n && it >= a.lv[k + 1].item_begin) ++k;   // items only increase
-    const ThreshLevel& L = a.lv[k];
-    const int rem = it - L.item_begin;
-    int y, j;
-    if (L.chunks) {          // wide: an item is 32 words of one row
-      y = L.chunks == 1 ? rem : rem / L.chunks;
-      j = (rem - y * L.chunks) * 32 + lane;
-      if (j >= L.nw32) continue;
-    } else {                 // narrow: an item is 32 consecutive words of the level (several rows)
-      const int f = rem * 32 + lane;
-      y = (int)__umulhi((uint32_t)f, L.magic);
-      j = f - y * L.nw32;
-      if (y >= L.h) continue;
-    }
-    const int x0 = 32 * j;
+  // One word: pack + store (word j of row y of level L; x0 = 32 j < w known).
+  auto word = [&](const ThreshLevel& L, int y, int j, bool in_px) {
     uint32_t mw = 0, ew = 0;
-    if (x0 < L.w) {
+    if (in_px) {
       // gray pitch is a multiple of 128 bytes: these 32 bytes are in-bounds and aligned.
-      const uint8_t* src = gray + L.gray_off + (int64_t)y * L.gray_pitch + x0;
+      const uint8_t* src = gray + L.gray_off + (int64_t)y * L.gray_pitch + 32 * j;
       const uint4* p = reinterpret_cast<const uint4*>(src);
       const uint4 v0 = __ldcs(p), v1 = __ldcs(p + 1);
       const uint32_t g[8] = {v0.x, v0.y, v0.z, v0.w, v1.x, v1.y, v1.z, v1.w};
       const ThConst c = s_th[k];
+      const int valid = L.w - 32 * j;
       if (c.med_lo) {
-        if (tol_lo) th_word_t<true, true>(g, c, yt, ytl, L.w - x0, mw, ew);
-        else th_word_t<true, false>(g, c, yt, ytl, L.w - x0, mw, ew);
+        if (tol_lo) th_word_t<true, true>(g, c, yt, ytl, valid, mw, ew);
+        else th_word_t<true, false>(g, c, yt, ytl, valid, mw, ew);
       } else {
-        if (tol_lo) th_word_t<false, true>(g, c, yt, ytl, L.w - x0, mw, ew);
-        else th_word_t<false, false>(g, c, yt, ytl, L.w - x0, mw, ew);
+        if (tol_lo) th_word_t<false, true>(g, c, yt, ytl, valid, mw, ew);
+        else th_word_t<false, false>(g, c, yt, ytl, valid, mw, ew);
       }
       if (a.discard && L.chunks) {
         // wide level: words j..j+3 share one 128-B line and are lanes of this
-        // item; drop the line from L2 (no write-back) once all of them read it
+        // warp; drop the line from L2 (no write-back) once all of them read it
         // (narrow levels keep theirs: a row's line may span two items).
         __syncwarp(__activemask());
         if ((j & 3) == 0) asm volatile("discard.global.L2 [%0], 128;" ::"l"(src) : "memory");
@@ -128,6 +114,24 @@ __global__ void __launch_bounds__(256, TH_MIN_BLOCKS) threshold_levels_kernel(Th
     const int64_t o = 2 * L.bit_off + (int64_t)y * L.nw32 + j;
     mtb[o] = mw;
     excl[o] = ew;
+  };
+  for (int it = blockIdx.x * wpc + (threadIdx.x >> 5); it < a.items; it += stride) {
+    while (k + 1 < a.n && it >= a.lv[k + 1].item_begin) ++k;   // items only increase
+    const ThreshLevel& L = a.lv[k];
+    const int rem = it - L.item_begin;
+    int y, j, jend;
+    if (L.chunks) {          // wide: an item is one row, lane j packs words j, j + 32, ...
+      y = rem;
+      j = lane;
+      jend = L.nw32;
+    } else {                 // narrow: an item is 32 consecutive words of the level (several rows)
+      const int f = rem * 32 + lane;
+      y = (int)__umulhi((uint32_t)f, L.magic);
+      j = f - y * L.nw32;
+      jend = y < L.h ? j + 1 : j;
+    }
+#pragma unroll 1
+    for (; j < jend; j += 32) word(L, y, j, 32 * j < L.w);
   }
 }
 
@@ -218,10 +222,10 @@ int launch_threshold_levels(const uint8_t* gray, const Plan& p, int n_img, const
     L.gray_pitch = p.lv[k].gray_pitch;
     L.bit_off = p.lv[k].bit_off;
     L.nw32 = (int)(2 * p.lv[k].nw64);
-    L.chunks = L.nw32 >= 32 ? (L.nw32 + 31) / 32 : 0;
+    L.chunks = L.nw32 >= 32 ? 1 : 0;
     L.magic = (uint32_t)((((uint64_t)1 << 32) + L.nw32 - 1) / L.nw32);   // exact for f < 2^32 / nw32
     L.item_begin = items;
-    items += L.chunks ? L.h * L.chunks : (L.h * L.nw32 + 31) / 32;
+    items += L.chunks ? L.h : (L.h * L.nw32 + 31) / 32;
   }
   a.items = items;
   a.mtb = reinterpret_cast<uint32_t*>(mtb);
