@@ -70,8 +70,10 @@ def parse():
     args.height = args.height or dflt["height"]
     args.pairs = args.pairs or dflt["units"]
     args.stack = dflt["stack"]
-    if args.config == 1 and "--mode" not in " ".join(sys.argv):
-        args.mode = "staged"   # small images: one persistent K1 launch over the batch wins
+    if "--mode" not in " ".join(sys.argv) and args.width * args.height < FUSED_MIN_PIXELS:
+        # the product's own dispatch (pipeline.use_fused): below ~13 MP the
+        # staged kernels win (one persistent K1 launch over the batch)
+        args.mode = "staged"
     return args
 
 
@@ -79,6 +81,8 @@ def parse():
 # `stack` images each (pairs: stack 2; config 3: 7-exposure stacks aligned to
 # their middle exposure, 6 pairs each).  Config 5 (one gigapixel pair,
 # row-sharded) is measured by tools/config5.py, not here.
+FUSED_MIN_PIXELS = 13_000_000   # = paper_2007_06483_b200.pipeline.FUSED_MIN_PIXELS (checked by tests)
+
 CONFIGS = {
     1: {"width": 1024, "height": 768, "units": 1024, "stack": 2},
     2: {"width": 6000, "height": 4000, "units": 64, "stack": 2},

@@ -7,9 +7,9 @@ behind it is batched on the device: every image's MTB pyramid and every
 pair's coarse-to-fine search run in one batched pass, the cumulative offsets
 are summed on the device and all outputs are shifted in one launch.
 
-Path selection (`use_fused`): images of >= 4 MP go through the fused
+Path selection (`use_fused`): images of >= 13 MP go through the fused
 pipeline (csrc/pipe.cu: preprocess and search of the whole stack in one
-pipelined launch sequence, 15 % faster at 24 MP); images whose gray pyramid
+pipelined launch sequence, 25 % faster at 24 MP); images whose gray pyramid
 fits the shared memory of a 1- or 2-CTA cluster (about 0.4 MP) through the
 on-chip preprocess (csrc/cluster.cu: one launch over the whole batch, gray
 never in HBM) and the batched search; the sizes between through the staged
@@ -124,7 +124,11 @@ def upload_stack(images):
     return host.to("cuda", non_blocking=True)
 
 
-FUSED_MIN_PIXELS = 4_000_000   # fused pipeline at >= 4 MP, staged kernels below
+# Fused pipeline at >= 13 MP, staged kernels below: the
+# pipeline's per-launch fixed costs need large images; measured at 128 pairs
+# per call: 6 MP staged 56.5 K vs fused 30.4 K pairs/s, 8 MP 42.9 K vs 29.1 K,
+# 12 MP 29.6 K both, 16 MP fused 25.7 K vs 23.5 K, 24 MP 18.3 K vs 14.7 K.
+FUSED_MIN_PIXELS = 13_000_000
 
 
 def use_fused(eng: MtbEngine) -> bool:

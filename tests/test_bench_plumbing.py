@@ -37,3 +37,10 @@ def test_halo_rows_cover_every_reachable_base():
             assert all(level_rows(r0, r1, k)[1] - level_rows(r0, r1, k)[0] > halo_rows(10, k) for r0, r1 in rows)
     with pytest.raises(ValueError):
         plan_row_shards(25000, 10, 25)   # 48 blocks < 2 per shard
+
+
+def test_bench_dispatch_threshold_matches_the_product():
+    import bench
+    from paper_2007_06483_b200 import pipeline
+
+    assert bench.FUSED_MIN_PIXELS == pipeline.FUSED_MIN_PIXELS

@@ -69,7 +69,9 @@ def test_config4_fused_vs_oracle(mtb, cuda):
 
     w, h = 4000, 3000
     eng = mtb.MtbEngine(w, h, 6, 4)
-    assert eng.fused_supported and mtb.pipeline.use_fused(eng)
+    # the API dispatches 12 MP to the staged kernels (equal speed there); the
+    # fused pipeline is tested directly at this size
+    assert eng.fused_supported and not mtb.pipeline.use_fused(eng)
     assert eng.fused_launches(4, [(0, 1), (2, 3)]) > 2
     imgs = []
     for s in range(2):
