@@ -109,13 +109,14 @@ def load_peak():
         return FALLBACK_HBM_GBS, "fallback (B200_PROFILING.md 6.65 TB/s)"
 
 
-def load_traffic(kernel: str):
-    """Per-launch DRAM bytes of `kernel` from the committed ncu summary, if any."""
+def load_traffic(kernel: str, width: int, height: int, images_per_launch: int):
+    """Per-launch DRAM bytes of `kernel` at this workload (W x H, images per
+    launch) from the committed ncu summary; None when no capture matches."""
     path = os.path.join(ROOT, "profiles", "ncu_summary.json")
     try:
         with open(path) as f:
             d = json.load(f)
-        return d["kernels"][kernel]
+        return d["by_workload"].get(f"{kernel}:{width}x{height}x{images_per_launch}")
     except Exception:
         return None
 
@@ -413,7 +414,9 @@ def run_ours(args, rank, world, local_rank):
         # pipe_kernel is 100 % of a fused step (ncu launch list, profiles/): its
         # achieved rate is the timed graph replays' algorithmic bytes / time
         achieved = n_img * img_bytes / (elapsed / args.steps) / 1e9
-    traffic = load_traffic("pipe_kernel" if fused else "k1_rgb_pyramid_kernel")
+    traffic = (load_traffic("pipe_kernel", args.width, args.height,
+                            _lib.load().mtb_align_fused_images_per_launch(args.width, args.height)) if fused else
+               load_traffic("k1_rgb_pyramid_kernel", args.width, args.height, k1_images))
     step_gbs = value / world * (n_img * img_bytes / P) / 1e9   # algorithmic bytes per pair = the step's RGB / pairs
 
     # every benched pair re-checked on the CPU (reference engine when built)

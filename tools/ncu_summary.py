@@ -98,6 +98,9 @@ def main():
             old = json.load(f)
         summary["kernels"].update(old.get("kernels", {}))
         summary["detail"].update(old.get("detail", {}))
+        for key in ("by_workload", "by_workload_note"):   # bench.py's roofline.traffic lookup
+            if key in old:
+                summary[key] = old[key]
     for k, ds in per_kernel.items():
         traffic = [d["dram__bytes_read.sum"] + d["dram__bytes_write.sum"] for d in ds]
         summary["kernels"][k] = round(sum(traffic) / len(traffic))
