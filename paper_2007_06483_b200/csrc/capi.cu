@@ -74,11 +74,11 @@ bool make_plan(int w, int h, int requested, Plan* p) {
 // Defined in pyramid.cu / threshold.cu.
 int64_t spread_hist_elems(int n_levels);
 int hist_bin_for(const Plan& p, int n_img);
+int hist_prepare(uint32_t* hist_ws, const Plan& p, int n_img, int hist_bin, cudaStream_t st);
 int launch_pyramid(const uint8_t* rgb, int64_t rgb_pitch, int64_t rgb_img_stride, int n_img, const Plan& p,
                    uint8_t* gray, uint32_t* spread_hist, int hist_bin, cudaStream_t st);
 int launch_hist_median(const uint32_t* spread_hist, int n_img, int n_levels, int hist_bin, uint32_t* dense,
                        int32_t* medians, cudaStream_t st);
-constexpr int kSpreadBin = 32;   // the split entry points keep the spread layout (sharded.py reads it)
 int launch_threshold_levels(const uint8_t* gray, const Plan& p, int n_img, const int32_t* medians, int tol,
                             uint64_t* mtb, uint64_t* excl, int discard, cudaStream_t st);
 
@@ -126,8 +126,10 @@ extern "C" int mtb_pyramid_hist(const uint8_t* rgb, int64_t rgb_pitch, int64_t r
   Plan p;
   MTB_REQUIRE(make_plan(w, h, levels, &p), "image must be at least 16x16 and levels >= 1");
   cudaStream_t st = as_stream(stream);
-  MTB_CUDA(cudaMemsetAsync(hist_ws, 0, sizeof(uint32_t) * spread_hist_elems(p.n) * n_img, st));
-  return launch_pyramid(rgb, rgb_pitch, rgb_img_stride, n_img, p, gray, hist_ws, kSpreadBin, st);
+  const int bin = hist_bin_for(p, n_img);
+  int rc = hist_prepare(hist_ws, p, n_img, bin, st);
+  if (rc) return rc;
+  return launch_pyramid(rgb, rgb_pitch, rgb_img_stride, n_img, p, gray, hist_ws, bin, st);
 }
 
 extern "C" int mtb_threshold_levels(const uint8_t* gray, const uint32_t* hist_ws, int w, int h, int n_img,
@@ -140,7 +142,7 @@ extern "C" int mtb_threshold_levels(const uint8_t* gray, const uint32_t* hist_ws
   Plan p;
   MTB_REQUIRE(make_plan(w, h, levels, &p), "image must be at least 16x16 and levels >= 1");
   cudaStream_t st = as_stream(stream);
-  int rc = launch_hist_median(hist_ws, n_img, p.n, kSpreadBin, hist_out, medians, st);
+  int rc = launch_hist_median(hist_ws, n_img, p.n, 0, hist_out, medians, st);   // layout from the marker
   if (rc) return rc;
   return launch_threshold_levels(gray, p, n_img, medians, tol, mtb, exclusion, discard_gray, st);
 }
@@ -158,8 +160,9 @@ extern "C" int mtb_preprocess(const uint8_t* rgb, int64_t rgb_pitch, int64_t rgb
   MTB_REQUIRE(make_plan(w, h, levels, &p), "image must be at least 16x16 and levels >= 1");
   cudaStream_t st = as_stream(stream);
   const int bin = hist_bin_for(p, n_img);
-  MTB_CUDA(cudaMemsetAsync(hist_ws, 0, sizeof(uint32_t) * (int64_t)p.n * 256 * bin * n_img, st));
-  int rc = launch_pyramid(rgb, rgb_pitch, rgb_img_stride, n_img, p, gray, hist_ws, bin, st);
+  int rc = hist_prepare(hist_ws, p, n_img, bin, st);
+  if (rc) return rc;
+  rc = launch_pyramid(rgb, rgb_pitch, rgb_img_stride, n_img, p, gray, hist_ws, bin, st);
   if (rc) return rc;
   rc = launch_hist_median(hist_ws, n_img, p.n, bin, hist_out, medians, st);
   if (rc) return rc;

@@ -238,7 +238,9 @@ __global__ void hist_median_kernel(const uint32_t* __restrict__ spread, int64_t 
   const int level = threadIdx.x >> 5;
   const int img = blockIdx.x;
   if (level >= n_levels) return;
-  const uint32_t* src = spread + img * spread_img_stride + (int64_t)level * 256 * bin;
+  const uint32_t* base = spread + img * spread_img_stride;
+  if (bin == 0) bin = base[spread_img_stride - 1] ? 1 : kHistStride;   // layout marker (hist_prepare)
+  const uint32_t* src = base + (int64_t)level * 256 * bin;
   uint32_t bins[8];
   unsigned long long s = 0;
 #pragma unroll
@@ -350,14 +352,31 @@ __global__ void median64_kernel(const unsigned long long* __restrict__ hist, int
 // Spread-histogram workspace needed by launch_pyramid (u32 elements / image).
 int64_t spread_hist_elems(int n_levels) { return (int64_t)n_levels * 256 * kHistStride; }
 
-// Bin stride of the staged histograms for one mtb_preprocess call: spread (one
-// 128-B line per bin) when many CTAs flush into one image's histogram, dense
-// when each CTA's tile range covers >= 2 whole images (the flushes of an
-// image then come from a handful of CTAs, and the 32x smaller workspace
-// saves the memset and the median pass ~200 MB per 1024 small images).
+// Bin stride of the staged histograms of one K1 launch: spread (one 128-B
+// line per bin) when many CTAs flush into one image's histogram, dense when
+// each CTA's tile range covers >= 2 whole images (the flushes of an image
+// then come from a handful of CTAs; the memset and the median pass touch
+// 32x less: ~200 MB less per 1024 small images).  Each image's workspace
+// region keeps the spread size; its LAST word records the layout (nonzero:
+// dense; in the spread layout it is an unused word of the last bin's line),
+// so mtb_threshold_levels reads the histograms right whatever call filled them.
 int hist_bin_for(const Plan& p, int n_img) {
   const int64_t tiles = (int64_t)((p.lv[0].w + 255) / 256) * ((p.lv[0].h + 31) / 32);
   return (int64_t)n_img * tiles >= 2 * tiles * num_sms() ? 1 : kHistStride;
+}
+
+// Zeroes the histogram workspace of n_img images for a K1 launch with this
+// bin stride and writes the per-image layout marker.
+int hist_prepare(uint32_t* hist_ws, const Plan& p, int n_img, int hist_bin, cudaStream_t st) {
+  const int64_t region = spread_hist_elems(p.n);
+  if (hist_bin == kHistStride) {
+    MTB_CUDA(cudaMemsetAsync(hist_ws, 0, sizeof(uint32_t) * region * n_img, st));
+  } else {
+    const size_t pitch = sizeof(uint32_t) * region;
+    MTB_CUDA(cudaMemset2DAsync(hist_ws, pitch, 0, sizeof(uint32_t) * (size_t)p.n * 256 * hist_bin, n_img, st));
+    MTB_CUDA(cudaMemset2DAsync(hist_ws + region - 1, pitch, 1, sizeof(uint32_t), n_img, st));
+  }
+  return MTB_OK;
 }
 
 // Builds gray levels 0..n-1 (plan p) and their spread histograms for n_img
@@ -371,7 +390,7 @@ bool k1_rgb_supported(int w, int64_t rgb_pitch, int64_t rgb_img_stride, const vo
 // tile passes over the deepest level produced so far (6 levels per pass).
 int launch_pyramid(const uint8_t* rgb, int64_t rgb_pitch, int64_t rgb_img_stride, int n_img,
                    const Plan& p, uint8_t* gray, uint32_t* spread_hist, int hist_bin, cudaStream_t st) {
-  const int64_t hist_img = (int64_t)p.n * 256 * hist_bin;
+  const int64_t hist_img = spread_hist_elems(p.n);   // per-image region; dense bins use its start
   // Interior tiles: the fast kernel (needs 16-B aligned RGB rows).  Edge
   // tiles (and every tile when rows are unaligned): the generic kernel.
   const bool vec_ok = k1_rgb_supported(p.lv[0].w, rgb_pitch, rgb_img_stride, rgb);
@@ -451,9 +470,12 @@ int launch_pyramid(const uint8_t* rgb, int64_t rgb_pitch, int64_t rgb_img_stride
   return launches ? check_launch("pyramid_tiles_kernel", launches) : MTB_OK;
 }
 
+// hist_bin 0: per image, from the layout marker hist_prepare left in the
+// region's last word (the split entry points cannot know the layout the
+// pyramid call chose).
 int launch_hist_median(const uint32_t* spread_hist, int n_img, int n_levels, int hist_bin, uint32_t* dense,
                        int32_t* medians, cudaStream_t st) {
-  hist_median_kernel<<<n_img, 32 * n_levels, 0, st>>>(spread_hist, (int64_t)n_levels * 256 * hist_bin, hist_bin,
+  hist_median_kernel<<<n_img, 32 * n_levels, 0, st>>>(spread_hist, spread_hist_elems(n_levels), hist_bin,
                                                       n_levels, dense, medians);
   return check_launch("hist_median_kernel");
 }

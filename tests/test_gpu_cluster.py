@@ -175,8 +175,13 @@ def test_dense_histograms_match_spread(mtb, cuda):
     batch = _batch(cuda, w, h, 8, 21).repeat(n // 8 + 1, 1, 1, 1)[:n].contiguous()
     dense = eng.preprocess(batch, keep_hist=True)          # one mtb_preprocess call: dense bins
     spread = eng.alloc(n, keep_hist=True)
-    eng.pyramid_hist(batch, spread)                         # split calls: spread bins
-    eng.threshold_levels(spread, n)
+    for i0 in range(0, n, 100):                             # K1 launches of 100 images: spread bins
+        eng.pyramid_hist(batch, spread, i0, 100)
+    eng.threshold_levels(spread, n)                         # one median pass, layout read per image
+    split_dense = eng.alloc(n, keep_hist=True)
+    eng.pyramid_hist(batch, split_dense)                    # one K1 launch of 300: dense bins
+    eng.threshold_levels(split_dense, n)
+    assert cuda.equal(split_dense.medians, spread.medians)
     assert cuda.equal(dense.medians, spread.medians)
     assert cuda.equal(dense.hist, spread.hist)
     for k in range(eng.n):
