@@ -22,6 +22,13 @@ __device__ __forceinline__ void cp_async4(uint32_t* dst, const uint32_t* src, bo
                : "memory");
 }
 
+// 16-byte global -> shared copy of `bytes` (0..16) leading bytes, zero-filled.
+__device__ __forceinline__ void cp_async16(uint32_t* dst, const uint32_t* src, int bytes) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"((uint32_t)__cvta_generic_to_shared(dst)),
+               "l"(src), "r"(bytes)
+               : "memory");
+}
+
 // Word idx of a packed row (u32 view), zero outside [0, nw32).
 __device__ __forceinline__ uint32_t row_word(const uint32_t* row, int64_t idx, int nw32) {
   return (idx >= 0 && idx < nw32) ? __ldg(row + idx) : 0u;
@@ -118,7 +125,7 @@ constexpr int kSTWarps = 8;          // 8 rows per warp
 constexpr int kSTThreads = kSTWarps * 32;
 constexpr int kSTBRows = kSTRows + 2;
 constexpr int kSTBWords = kSTWords + 3;
-constexpr int kSTBPitch = kSTBWords + 1;
+constexpr int kSTBPitch = 40;        // 16-B rows: staged by 16-B copies from a 4-word-aligned origin
 
 struct LevelSearchArgs {
   const uint64_t* const* maps;   // [P][4] {ref.mtb, ref.excl, tgt.mtb, tgt.excl}
@@ -149,7 +156,7 @@ struct LevelSearchArgs {
   int seg_row0[3], seg_rows[3];
 };
 
-struct SearchSmem {
+struct __align__(16) SearchSmem {
   uint32_t a[kSTRows][kSTWords];
   uint32_t ea[kSTRows][kSTWords];
   uint32_t b[kSTBRows][kSTBPitch];
@@ -176,11 +183,66 @@ __device__ __forceinline__ unsigned long long search_tile(const LevelSearchArgs&
   const int sy0 = y0 - by - 1;           // first staged source row
   const int64_t sj0 = (int64_t)j0 - qb - 2;  // first staged source word
 
-  // ---- stage: global -> shared by 4-byte cp.async (zero-filled outside the
-  // maps), all copies in flight together.  Warp wi stages rows wi, wi + 8, ...
-  // (row validity and the row pointer are warp-uniform), lane = word; the
-  // target halo's words 32..34 go to lanes 0..2. ----
-  {
+  // ---- stage: global -> shared by cp.async (zero-filled outside the maps),
+  // all copies in flight together.  Rows of 16-B multiples (nw32 % 4 == 0,
+  // the common case): 16-B copies, the target halo from the 4-word-aligned
+  // word at or left of sj0 (staged column `mis` = word sj0), partial edge
+  // chunks word by word.  Otherwise 4-byte copies: warp wi stages rows wi,
+  // wi + 8, ... (row validity and pointer warp-uniform), lane = word, the
+  // halo's words 32..34 by lanes 0..2. ----
+  int mis = 0;
+  auto b_row = [&](int64_t y, const uint32_t*& pm, const uint32_t*& pe) {
+    pm = nullptr;
+    pe = nullptr;
+    if (y >= 0 && y < a.h) {
+      if (SEG) {
+#pragma unroll
+        for (int sg = 0; sg < 3; ++sg)
+          if (a.seg_m[sg] && y >= a.seg_row0[sg] && y < (int64_t)a.seg_row0[sg] + a.seg_rows[sg]) {
+            pm = a.seg_m[sg] + (y - a.seg_row0[sg]) * a.nw32;
+            pe = a.seg_e[sg] + (y - a.seg_row0[sg]) * a.nw32;
+          }
+      } else if (y >= a.b_row0 && y < a.b_row0 + a.b_rows) {
+        pm = B + (y - a.b_row0) * a.nw32;
+        pe = EB + (y - a.b_row0) * a.nw32;
+      }
+    }
+  };
+  if ((a.nw32 & 3) == 0) {
+#pragma unroll
+    for (int k = 0; k < kSTRows * kSTWords / 4 / kSTThreads; ++k) {
+      const int c = tid + kSTThreads * k, r = c >> 3, q = c & 7;
+      const int ly = ly0 + r, w = j0 + 4 * q;
+      const int nb = ly < a.a_rows ? max(0, min(16, 4 * (a.nw32 - w))) : 0;
+      const int64_t o = nb ? (int64_t)ly * a.nw32 + w : 0;
+      cp_async16(&S.a[r][4 * q], A + o, nb);
+      cp_async16(&S.ea[r][4 * q], EA + o, nb);
+    }
+    const int64_t bw0 = sj0 & ~(int64_t)3;
+    mis = (int)(sj0 - bw0);
+    constexpr int kChunks = kSTBPitch / 4;   // 10 x 4 words per staged row
+    for (int c = tid; c < kSTBRows * kChunks; c += kSTThreads) {
+      const int r = c / kChunks, q = c - r * kChunks;
+      const uint32_t* pm;
+      const uint32_t* pe;
+      b_row((int64_t)sy0 + r, pm, pe);
+      const int64_t w = bw0 + 4 * q;
+      if (pm && w >= 0 && w + 4 <= a.nw32) {
+        cp_async16(&S.b[r][4 * q], pm + w, 16);
+        cp_async16(&S.eb[r][4 * q], pe + w, 16);
+      } else if (!pm || w + 4 <= 0 || w >= a.nw32) {
+        cp_async16(&S.b[r][4 * q], A, 0);
+        cp_async16(&S.eb[r][4 * q], A, 0);
+      } else {
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          const bool ok = w + i >= 0 && w + i < a.nw32;
+          cp_async4(&S.b[r][4 * q + i], ok ? pm + w + i : A, ok);
+          cp_async4(&S.eb[r][4 * q + i], ok ? pe + w + i : A, ok);
+        }
+      }
+    }
+  } else {
     const int jA = j0 + lane;
     const bool colA = jA < a.nw32;
 #pragma unroll
@@ -198,22 +260,9 @@ __device__ __forceinline__ unsigned long long search_tile(const LevelSearchArgs&
     for (int k = 0; k < (kSTBRows + kSTWarps - 1) / kSTWarps; ++k) {
       const int r = wi + kSTWarps * k;
       if (r >= kSTBRows) break;
-      const int64_t y = (int64_t)sy0 + r;
-      const uint32_t* pm = nullptr;
-      const uint32_t* pe = nullptr;
-      if (y >= 0 && y < a.h) {
-        if (SEG) {
-#pragma unroll
-          for (int sg = 0; sg < 3; ++sg)
-            if (a.seg_m[sg] && y >= a.seg_row0[sg] && y < (int64_t)a.seg_row0[sg] + a.seg_rows[sg]) {
-              pm = a.seg_m[sg] + (y - a.seg_row0[sg]) * a.nw32;
-              pe = a.seg_e[sg] + (y - a.seg_row0[sg]) * a.nw32;
-            }
-        } else if (y >= a.b_row0 && y < a.b_row0 + a.b_rows) {
-          pm = B + (y - a.b_row0) * a.nw32;
-          pe = EB + (y - a.b_row0) * a.nw32;
-        }
-      }
+      const uint32_t* pm;
+      const uint32_t* pe;
+      b_row((int64_t)sy0 + r, pm, pe);
       const bool row = pm != nullptr;
       if (!row) {
         pm = A;
@@ -226,8 +275,8 @@ __device__ __forceinline__ unsigned long long search_tile(const LevelSearchArgs&
         cp_async4(&S.eb[r][32 + lane], pe + (row && cb1 ? jb1 : 0), row && cb1);
       }
     }
-    asm volatile("cp.async.wait_all;" ::: "memory");
   }
+  asm volatile("cp.async.wait_all;" ::: "memory");
   __syncthreads();
 
   // ---- compute: warp wi -> output rows 8wi .. 8wi+7, lane -> word ----
@@ -240,16 +289,17 @@ __device__ __forceinline__ unsigned long long search_tile(const LevelSearchArgs&
   for (int i = 0; i < 9; ++i) cnt[i] = 0;
   const int rbeg = wi * (kSTRows / kSTWarps);
   const int rbx = bx & 31;
+  const int lm = lane + mis;   // staged column of source word j0 + lane - qb - 2
   auto rows = [&](auto case_tag) {
     constexpr int CASE = decltype(case_tag)::value;   // 0: rbx == 0, 1: rbx == 31, 2: other
     const int r0 = CASE == 0 ? 31 : (CASE == 1 ? 30 : rbx - 1);
     const int r1 = CASE == 0 ? 0 : (CASE == 1 ? 31 : rbx);
     const int r2 = CASE == 0 ? 1 : (CASE == 1 ? 0 : rbx + 1);
     auto shifted_row = [&](int lb, uint32_t (&sb)[3], uint32_t (&se)[3]) {
-      const uint32_t w0 = S.b[lb][lane], w1 = S.b[lb][lane + 1], w2 = S.b[lb][lane + 2];
-      const uint32_t v0 = S.eb[lb][lane], v1 = S.eb[lb][lane + 1], v2 = S.eb[lb][lane + 2];
+      const uint32_t w0 = S.b[lb][lm], w1 = S.b[lb][lm + 1], w2 = S.b[lb][lm + 2];
+      const uint32_t v0 = S.eb[lb][lm], v1 = S.eb[lb][lm + 1], v2 = S.eb[lb][lm + 2];
       if (CASE == 0) {
-        const uint32_t w3 = S.b[lb][lane + 3], v3 = S.eb[lb][lane + 3];
+        const uint32_t w3 = S.b[lb][lm + 3], v3 = S.eb[lb][lm + 3];
         sb[0] = shifted_word(w2, w3, r0); se[0] = shifted_word(v2, v3, r0);
       } else {
         sb[0] = shifted_word(w1, w2, r0); se[0] = shifted_word(v1, v2, r0);
