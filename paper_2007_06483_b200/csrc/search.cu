@@ -22,11 +22,17 @@ __device__ __forceinline__ void cp_async4(uint32_t* dst, const uint32_t* src, bo
                : "memory");
 }
 
-// 16-byte global -> shared copy of `bytes` (0..16) leading bytes, zero-filled.
-__device__ __forceinline__ void cp_async16(uint32_t* dst, const uint32_t* src, int bytes) {
-  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"((uint32_t)__cvta_generic_to_shared(dst)),
-               "l"(src), "r"(bytes)
-               : "memory");
+// CW-word (16 or 8 byte) global -> shared copy of `bytes` leading bytes, zero-filled.
+template <int CW>
+__device__ __forceinline__ void cp_async_n(uint32_t* dst, const uint32_t* src, int bytes) {
+  if constexpr (CW == 4)
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"((uint32_t)__cvta_generic_to_shared(dst)),
+                 "l"(src), "r"(bytes)
+                 : "memory");
+  else
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;" ::"r"((uint32_t)__cvta_generic_to_shared(dst)),
+                 "l"(src), "r"(bytes)
+                 : "memory");
 }
 
 // Word idx of a packed row (u32 view), zero outside [0, nw32).
@@ -124,8 +130,9 @@ constexpr int kSTWords = 32;         // output words per tile
 constexpr int kSTWarps = 8;          // 8 rows per warp
 constexpr int kSTThreads = kSTWarps * 32;
 constexpr int kSTBRows = kSTRows + 2;
-constexpr int kSTBWords = kSTWords + 3;
-constexpr int kSTBPitch = 40;        // 16-B rows: staged by 16-B copies from a 4-word-aligned origin
+// target rows staged: the tile's 32 words plus halo (2 left, 1 right) = 35,
+// from an origin up to 3 words further left (16-B aligned copies): 40 words
+constexpr int kSTBPitch = 40;
 
 struct LevelSearchArgs {
   const uint64_t* const* maps;   // [P][4] {ref.mtb, ref.excl, tgt.mtb, tgt.excl}
@@ -184,12 +191,10 @@ __device__ __forceinline__ unsigned long long search_tile(const LevelSearchArgs&
   const int64_t sj0 = (int64_t)j0 - qb - 2;  // first staged source word
 
   // ---- stage: global -> shared by cp.async (zero-filled outside the maps),
-  // all copies in flight together.  Rows of 16-B multiples (nw32 % 4 == 0,
-  // the common case): 16-B copies, the target halo from the 4-word-aligned
-  // word at or left of sj0 (staged column `mis` = word sj0), partial edge
-  // chunks word by word.  Otherwise 4-byte copies: warp wi stages rows wi,
-  // wi + 8, ... (row validity and pointer warp-uniform), lane = word, the
-  // halo's words 32..34 by lanes 0..2. ----
+  // all copies in flight together, in chunks of CW words: 16 B when rows are
+  // 16-byte multiples (nw32 % 4 == 0), else 8 B (rows are whole u64 words).
+  // The target halo is staged from the CW-aligned word at or left of sj0
+  // (staged column `mis` holds word sj0); partial edge chunks go word by word. ----
   int mis = 0;
   auto b_row = [&](int64_t y, const uint32_t*& pm, const uint32_t*& pe) {
     pm = nullptr;
@@ -208,74 +213,47 @@ __device__ __forceinline__ unsigned long long search_tile(const LevelSearchArgs&
       }
     }
   };
-  if ((a.nw32 & 3) == 0) {
+  auto stage = [&](auto cw_tag) {
+    constexpr int CW = decltype(cw_tag)::value;   // words per copy: 4 or 2
+    constexpr int CA = kSTWords / CW;               // chunks per reference row
 #pragma unroll
-    for (int k = 0; k < kSTRows * kSTWords / 4 / kSTThreads; ++k) {
-      const int c = tid + kSTThreads * k, r = c >> 3, q = c & 7;
-      const int ly = ly0 + r, w = j0 + 4 * q;
-      const int nb = ly < a.a_rows ? max(0, min(16, 4 * (a.nw32 - w))) : 0;
+    for (int k = 0; k < kSTRows * CA / kSTThreads; ++k) {
+      const int c = tid + kSTThreads * k, r = c / CA, q = c - r * CA;
+      const int ly = ly0 + r, w = j0 + CW * q;
+      const int nb = ly < a.a_rows ? max(0, min(4 * CW, 4 * (a.nw32 - w))) : 0;
       const int64_t o = nb ? (int64_t)ly * a.nw32 + w : 0;
-      cp_async16(&S.a[r][4 * q], A + o, nb);
-      cp_async16(&S.ea[r][4 * q], EA + o, nb);
+      cp_async_n<CW>(&S.a[r][CW * q], A + o, nb);
+      cp_async_n<CW>(&S.ea[r][CW * q], EA + o, nb);
     }
-    const int64_t bw0 = sj0 & ~(int64_t)3;
+    const int64_t bw0 = sj0 & ~(int64_t)(CW - 1);
     mis = (int)(sj0 - bw0);
-    constexpr int kChunks = kSTBPitch / 4;   // 10 x 4 words per staged row
-    for (int c = tid; c < kSTBRows * kChunks; c += kSTThreads) {
-      const int r = c / kChunks, q = c - r * kChunks;
+    constexpr int CB = kSTBPitch / CW;   // chunks per staged target row
+    for (int c = tid; c < kSTBRows * CB; c += kSTThreads) {
+      const int r = c / CB, q = c - r * CB;
       const uint32_t* pm;
       const uint32_t* pe;
       b_row((int64_t)sy0 + r, pm, pe);
-      const int64_t w = bw0 + 4 * q;
-      if (pm && w >= 0 && w + 4 <= a.nw32) {
-        cp_async16(&S.b[r][4 * q], pm + w, 16);
-        cp_async16(&S.eb[r][4 * q], pe + w, 16);
-      } else if (!pm || w + 4 <= 0 || w >= a.nw32) {
-        cp_async16(&S.b[r][4 * q], A, 0);
-        cp_async16(&S.eb[r][4 * q], A, 0);
+      const int64_t w = bw0 + CW * q;
+      if (pm && w >= 0 && w + CW <= a.nw32) {
+        cp_async_n<CW>(&S.b[r][CW * q], pm + w, 4 * CW);
+        cp_async_n<CW>(&S.eb[r][CW * q], pe + w, 4 * CW);
+      } else if (!pm || w + CW <= 0 || w >= a.nw32) {
+        cp_async_n<CW>(&S.b[r][CW * q], A, 0);
+        cp_async_n<CW>(&S.eb[r][CW * q], A, 0);
       } else {
 #pragma unroll
-        for (int i = 0; i < 4; ++i) {
+        for (int i = 0; i < CW; ++i) {
           const bool ok = w + i >= 0 && w + i < a.nw32;
-          cp_async4(&S.b[r][4 * q + i], ok ? pm + w + i : A, ok);
-          cp_async4(&S.eb[r][4 * q + i], ok ? pe + w + i : A, ok);
+          cp_async4(&S.b[r][CW * q + i], ok ? pm + w + i : A, ok);
+          cp_async4(&S.eb[r][CW * q + i], ok ? pe + w + i : A, ok);
         }
       }
     }
-  } else {
-    const int jA = j0 + lane;
-    const bool colA = jA < a.nw32;
-#pragma unroll
-    for (int k = 0; k < kSTRows / kSTWarps; ++k) {
-      const int r = wi + kSTWarps * k, ly = ly0 + r;
-      const bool ok = colA && ly < a.a_rows;
-      const int64_t o = ok ? (int64_t)ly * a.nw32 + jA : 0;
-      cp_async4(&S.a[r][lane], A + o, ok);
-      cp_async4(&S.ea[r][lane], EA + o, ok);
-    }
-    const int64_t jb0 = sj0 + lane, jb1 = sj0 + 32 + lane;
-    const bool cb0 = jb0 >= 0 && jb0 < a.nw32;
-    const bool cb1 = lane < kSTBWords - 32 && jb1 >= 0 && jb1 < a.nw32;
-#pragma unroll
-    for (int k = 0; k < (kSTBRows + kSTWarps - 1) / kSTWarps; ++k) {
-      const int r = wi + kSTWarps * k;
-      if (r >= kSTBRows) break;
-      const uint32_t* pm;
-      const uint32_t* pe;
-      b_row((int64_t)sy0 + r, pm, pe);
-      const bool row = pm != nullptr;
-      if (!row) {
-        pm = A;
-        pe = EA;
-      }
-      cp_async4(&S.b[r][lane], pm + (row && cb0 ? jb0 : 0), row && cb0);
-      cp_async4(&S.eb[r][lane], pe + (row && cb0 ? jb0 : 0), row && cb0);
-      if (lane < kSTBWords - 32) {
-        cp_async4(&S.b[r][32 + lane], pm + (row && cb1 ? jb1 : 0), row && cb1);
-        cp_async4(&S.eb[r][32 + lane], pe + (row && cb1 ? jb1 : 0), row && cb1);
-      }
-    }
-  }
+  };
+  if ((a.nw32 & 3) == 0)
+    stage(std::integral_constant<int, 4>{});
+  else
+    stage(std::integral_constant<int, 2>{});
   asm volatile("cp.async.wait_all;" ::: "memory");
   __syncthreads();
 
