@@ -503,7 +503,8 @@ def oracle_check(args, torch, batch, pairs, acc, errs):
 
     acc_h, errs_h = acc.cpu().numpy(), errs.cpu().numpy()
     imgs_needed = sorted({i for p in pairs for i in p})
-    workers = os.cpu_count() or 1
+    # ranks of a multi-GPU run share the host's cores
+    workers = max(1, (os.cpu_count() or 1) // int(os.environ.get("WORLD_SIZE", "1")))
     pyrs = {}
     with cf.ThreadPoolExecutor(max_workers=workers) as pool:
         futs = {}
