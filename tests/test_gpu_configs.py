@@ -84,6 +84,27 @@ def test_config4_fused_vs_oracle(mtb, cuda):
     _check_traces(acc, errs, pre, [(0, 1), (2, 3)])
 
 
+def test_config4_staged_vs_oracle(mtb, cuda):
+    """4000 x 3000 through the staged kernels the API dispatches 12 MP to:
+    rows of 63 u64 words (the search stages 8-byte chunks), offsets up to 63
+    px (halo chunks past both row ends), medians, maps and every trace."""
+    from paper_2007_06483_b200.synth import generate_stack, synthetic_rgb_device
+
+    w, h = 4000, 3000
+    eng = mtb.MtbEngine(w, h, 6, 4)
+    assert not mtb.pipeline.use_fused(eng) and (int(eng.geom[0, 4]) * 2) % 4 == 2
+    imgs = []
+    for s in range(2):
+        st, _ = generate_stack(synthetic_rgb_device(50 + s, w, h), 2, seed=50 + s, max_shift=63)
+        imgs += st
+    batch = cuda.stack(imgs).contiguous()
+    pyr = eng.preprocess(batch)
+    acc, errs = eng.search(pyr, [(0, 1), (2, 3)])
+    host = [im.cpu().numpy() for im in imgs]
+    pre = _check_pre(eng, pyr, host, 6)
+    _check_traces(acc, errs, pre, [(0, 1), (2, 3)])
+
+
 def test_config3_pivot_stack_fused_vs_oracle(mtb, cuda):
     """7 x 6000 x 4000 aligned to exposure 3 (SURVEY 8(d) config 3 recipe) via
     align(mode="pivot"): offsets, every trace and the aligned outputs."""
