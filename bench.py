@@ -70,10 +70,9 @@ def parse():
     args.height = args.height or dflt["height"]
     args.pairs = args.pairs or dflt["units"]
     args.stack = dflt["stack"]
-    if "--mode" not in " ".join(sys.argv) and args.width * args.height < FUSED_MIN_PIXELS:
-        # the product's own dispatch (pipeline.use_fused): below ~13 MP the
-        # staged kernels win (one persistent K1 launch over the batch)
-        args.mode = "staged"
+    if "--mode" not in " ".join(sys.argv):
+        # the product's own dispatch (pipeline.use_fused)
+        args.mode = "fused" if fused_default(args.width, args.height, args.pairs * args.stack) else "staged"
     return args
 
 
@@ -81,7 +80,17 @@ def parse():
 # `stack` images each (pairs: stack 2; config 3: 7-exposure stacks aligned to
 # their middle exposure, 6 pairs each).  Config 5 (one gigapixel pair,
 # row-sharded) is measured by tools/config5.py, not here.
-FUSED_MIN_PIXELS = 13_000_000   # = paper_2007_06483_b200.pipeline.FUSED_MIN_PIXELS (checked by tests)
+# = paper_2007_06483_b200.pipeline's dispatch tables (checked by tests)
+FUSED_MIN_PIXELS = 13_000_000
+FUSED_MIN_IMAGES = {20_000_000: 20, FUSED_MIN_PIXELS: 96}
+
+
+def fused_default(width: int, height: int, n_img: int) -> bool:
+    for min_px, min_img in sorted(FUSED_MIN_IMAGES.items(), reverse=True):
+        if width * height >= min_px:
+            return n_img >= min_img
+    return False
+
 
 CONFIGS = {
     1: {"width": 1024, "height": 768, "units": 1024, "stack": 2},

@@ -7,9 +7,10 @@ behind it is batched on the device: every image's MTB pyramid and every
 pair's coarse-to-fine search run in one batched pass, the cumulative offsets
 are summed on the device and all outputs are shifted in one launch.
 
-Path selection (`use_fused`): images of >= 13 MP go through the fused
-pipeline (csrc/pipe.cu: preprocess and search of the whole stack in one
-pipelined launch sequence, 25 % faster at 24 MP); images whose gray pyramid
+Path selection (`use_fused`): batches of >= 20 images of >= 20 MP (or >= 96
+of >= 13 MP) go through the fused pipeline (csrc/pipe.cu: preprocess and
+search of the whole stack in one pipelined launch sequence, 25 % faster for
+64 pairs of 24 MP); images whose gray pyramid
 fits the shared memory of a 1- or 2-CTA cluster (about 0.4 MP) through the
 on-chip preprocess (csrc/cluster.cu: one launch over the whole batch, gray
 never in HBM) and the batched search; the sizes between through the staged
@@ -124,16 +125,28 @@ def upload_stack(images):
     return host.to("cuda", non_blocking=True)
 
 
-# Fused pipeline at >= 13 MP, staged kernels below: the
-# pipeline's per-launch fixed costs need large images; measured at 128 pairs
-# per call: 6 MP staged 56.5 K vs fused 30.4 K pairs/s, 8 MP 42.9 K vs 29.1 K,
-# 12 MP 29.6 K both, 16 MP fused 25.7 K vs 23.5 K, 24 MP 18.3 K vs 14.7 K.
+# Fused pipeline or staged kernels.  The pipeline's
+# per-launch fixed costs pay only for large images in large batches:
+#   pairs/s at 128 pairs per call: 6 MP staged 56.5 K vs fused 30.4 K, 8 MP
+#   42.9 K vs 29.1 K, 12 MP 29.6 K both, 16 MP fused 25.7 K vs 23.5 K, 24 MP
+#   18.3 K vs 14.7 K;
+#   call latency of n-image chains: 24 MP staged faster up to 13 images
+#   (2: 0.16 vs 0.22 ms, 13: 0.54 vs 0.57 ms), fused from 25 (0.93 vs 0.96);
+#   16 MP staged up to ~50 images, even at 97.
 FUSED_MIN_PIXELS = 13_000_000
+FUSED_MIN_IMAGES = {20_000_000: 20, FUSED_MIN_PIXELS: 96}   # image size -> batch size from which fused wins
 
 
-def use_fused(eng: MtbEngine) -> bool:
-    """True when the fused pipeline is the faster path for this engine's images."""
-    return eng.fused_supported and eng.width * eng.height >= FUSED_MIN_PIXELS
+def use_fused(eng: MtbEngine, n_img: int) -> bool:
+    """True when the fused pipeline is the faster path for a call of n_img of
+    this engine's images."""
+    if not eng.fused_supported:
+        return False
+    px = eng.width * eng.height
+    for min_px, min_img in sorted(FUSED_MIN_IMAGES.items(), reverse=True):
+        if px >= min_px:
+            return n_img >= min_img
+    return False
 
 
 class _StageClock:
@@ -175,7 +188,7 @@ def _pairs_for(n: int, mode: str, pivot):
 def _run_batch(eng: MtbEngine, batch, pairs, clk: _StageClock):
     """Preprocess + search of a device batch; marks pyramid / threshold / search."""
     n_img = int(batch.shape[0])
-    if use_fused(eng):
+    if use_fused(eng, n_img):
         _, acc, errs = eng.align_fused(batch, pairs)
         clk.mark()          # pyramid: the whole pipelined sequence
         clk.mark()          # threshold: inside it
@@ -329,7 +342,7 @@ def get_exp_shift(ref_rgb, tgt_rgb, levels: int = DEFAULT_LEVELS, tol: int = DEF
     w, h = _validate_stack([ref_rgb, tgt_rgb])
     eng = engine_for(w, h, levels, tol)
     batch = upload_stack([ref_rgb, tgt_rgb])
-    if use_fused(eng):
+    if use_fused(eng, 2):   # (never, with the measured thresholds: one pair is faster staged)
         _, acc, _ = eng.align_fused(batch, [(0, 1)])     # one pipelined launch sequence (csrc/pipe.cu)
     else:
         pyr = eng.preprocess(batch, maps_only=True)
@@ -364,7 +377,7 @@ def align_files(paths, levels: int = DEFAULT_LEVELS, tol: int = DEFAULT_NOISE_TO
     if w < MIN_LEVEL_SIZE or h < MIN_LEVEL_SIZE:
         raise ValueError(f"images must be at least 16x16; got {w}x{h}")
     eng = engine_for(w, h, levels, tol)
-    if use_fused(eng):
+    if use_fused(eng, n):
         batch, _, acc, errs = eng.align_fused_host(host, pairs)
     else:
         batch = host.to("cuda", non_blocking=True)

@@ -44,3 +44,9 @@ def test_bench_dispatch_threshold_matches_the_product():
     from paper_2007_06483_b200 import pipeline
 
     assert bench.FUSED_MIN_PIXELS == pipeline.FUSED_MIN_PIXELS
+    assert bench.FUSED_MIN_IMAGES == pipeline.FUSED_MIN_IMAGES
+    cfg = bench.CONFIGS
+    assert bench.fused_default(cfg[2]["width"], cfg[2]["height"], cfg[2]["units"] * cfg[2]["stack"])
+    assert bench.fused_default(cfg[3]["width"], cfg[3]["height"], cfg[3]["units"] * cfg[3]["stack"])
+    assert not bench.fused_default(cfg[4]["width"], cfg[4]["height"], cfg[4]["units"] * cfg[4]["stack"])
+    assert not bench.fused_default(cfg[1]["width"], cfg[1]["height"], cfg[1]["units"] * cfg[1]["stack"])

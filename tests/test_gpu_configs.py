@@ -71,7 +71,7 @@ def test_config4_fused_vs_oracle(mtb, cuda):
     eng = mtb.MtbEngine(w, h, 6, 4)
     # the API dispatches 12 MP to the staged kernels (equal speed there); the
     # fused pipeline is tested directly at this size
-    assert eng.fused_supported and not mtb.pipeline.use_fused(eng)
+    assert eng.fused_supported and not mtb.pipeline.use_fused(eng, 4)
     assert eng.fused_launches(4, [(0, 1), (2, 3)]) > 2
     imgs = []
     for s in range(2):
@@ -92,7 +92,7 @@ def test_config4_staged_vs_oracle(mtb, cuda):
 
     w, h = 4000, 3000
     eng = mtb.MtbEngine(w, h, 6, 4)
-    assert not mtb.pipeline.use_fused(eng) and (int(eng.geom[0, 4]) * 2) % 4 == 2
+    assert not mtb.pipeline.use_fused(eng, 4) and (int(eng.geom[0, 4]) * 2) % 4 == 2
     imgs = []
     for s in range(2):
         st, _ = generate_stack(synthetic_rgb_device(50 + s, w, h), 2, seed=50 + s, max_shift=63)
@@ -107,7 +107,8 @@ def test_config4_staged_vs_oracle(mtb, cuda):
 
 def test_config3_pivot_stack_fused_vs_oracle(mtb, cuda):
     """7 x 6000 x 4000 aligned to exposure 3 (SURVEY 8(d) config 3 recipe) via
-    align(mode="pivot"): offsets, every trace and the aligned outputs."""
+    align(mode="pivot") (staged for one stack) and the fused pipeline:
+    offsets, every trace and the aligned outputs."""
     from paper_2007_06483_b200.synth import generate_stack, synthetic_rgb_device
 
     w, h = 6000, 4000
@@ -115,10 +116,14 @@ def test_config3_pivot_stack_fused_vs_oracle(mtb, cuda):
     imgs, man = generate_stack(base, 7, seed=2, max_shift=20, gains=[2 ** ((k - 3) / 3) for k in range(7)],
                                gammas=[1.0] * 7)
     eng = mtb.pipeline.engine_for(w, h, 6, 4)
-    assert mtb.pipeline.use_fused(eng)
+    assert not mtb.pipeline.use_fused(eng, 7)   # one 7-stack: staged is the faster call
     aligned, rec = mtb.align(imgs, mode="pivot")
     host = [im.cpu().numpy() for im in imgs]
     pre = [orc.preprocess(im, 6, 4) for im in host]
+    # the fused pipeline on the same stack (what config 3's batches of 16 stacks use)
+    pivot = [(3, i) for i in range(7) if i != 3]
+    _, facc, ferrs = eng.align_fused(cuda.stack(imgs).contiguous(), pivot)
+    _check_traces(facc, ferrs, pre, pivot)
     for (ref, tgt), res in zip([(3, i) for i in range(7) if i != 3], rec.pairwise):
         want = orc.find_offset(pre[ref]["mtb"], pre[tgt]["mtb"])
         assert tuple(res.offset) == tuple(want["offset"]), (tgt, res.offset, want["offset"])
@@ -232,7 +237,7 @@ def test_stage_timings_from_events(mtb, cuda):
         assert all(v >= 0.0 for v in rec.timings.values())
         total = sum(rec.timings.values())
         assert total <= wall * 1.05 + 1.0 and total >= wall * 0.5, (total, wall)
-        if w * h >= 4_000_000:
+        if mtb.pipeline.use_fused(mtb.pipeline.engine_for(w, h, 6, 4), len(imgs)):
             assert rec.timings["threshold"] == pytest.approx(0.0, abs=0.05)
 
 
