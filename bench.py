@@ -555,7 +555,7 @@ def single_pair_latency(torch, mtb, batch):
         e.synchronize()
         times.append(s.elapsed_time(e))
     return {"ms_median": round(statistics.median(times), 4), "ms_best": round(min(times), 4),
-            "api": "get_exp_shift (fused pipeline, device-resident pair, includes the offset readback)"}
+            "api": "get_exp_shift (its own dispatch: staged kernels for one pair; device-resident pair, includes the offset readback)"}
 
 
 def _world_max_time(dt):
